@@ -1,0 +1,59 @@
+// Host-visible declarations for the tcgen05 GEMM (D = A . B^T, bf16 in, fp32 acc) with the
+// fused STDiT epilogues. Layout contract: A [M, K] row-major (K contiguous, row stride lda),
+// B [N, K] row-major (nn.Linear weight layout), both staged K-major by TMA with the 128 B swizzle.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ddit {
+
+enum EpiKind : int {
+  EPI_BF16 = 0,       // out_bf16 = acc + bias
+  EPI_GELU_BF16 = 1,  // out_bf16 = gelu_tanh(acc + bias)
+  EPI_RESID = 2,      // resid_f32 += gate[b] * (acc + bias)   (gate == null -> 1); optional bf16 copy
+  EPI_QKV = 3,        // out_bf16 = rope(rmsnorm_head(acc + bias)) on the q/k sections; v: acc + bias
+  EPI_F32 = 4,        // out_f32 = acc + bias
+};
+
+struct EpiParams {
+  const float* bias;        // [N] or null
+  void* out;                // bf16 [M, ldo] (EPI_F32: fp32)
+  int ldo;
+  float* resid;             // EPI_RESID: fp32 [M, ldr]
+  int ldr;
+  const float* gate;        // EPI_RESID: [B][gate_stride] or null
+  int gate_stride;
+  int rows_per_b;           // row -> batch index b = row / rows_per_b
+  __nv_bfloat16* out2;      // EPI_RESID: optional bf16 copy of the updated residual [M, ldo2]
+  int ldo2;
+  // EPI_QKV
+  const float* qnorm_w;     // [head_dim]
+  const float* knorm_w;     // [head_dim]
+  int hidden;               // C: q = [0,C), k = [C,2C), v = [2C,3C)
+  int rope;                 // 1: rotate q,k by frame position
+  int rope_T;               // number of frames
+  int rope_S;               // tokens per frame in this row layout: t = (row / rope_S) % rope_T
+  const float2* rope_tab;   // [rope_T][head_dim/2] (cos, sin)
+  float eps;
+};
+
+struct GemmPlan {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  int M, N, K;
+  int bn;
+  int epi;
+  EpiParams ep;
+  int grid;
+};
+
+// Build the TMA descriptors and launch geometry. Returns 0 on success.
+int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
+                   int K, int epi, const EpiParams& ep, int bn);
+int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
+int num_sms();
+const char* gemm_last_error();
+
+}  // namespace ddit

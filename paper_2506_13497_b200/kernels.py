@@ -1,0 +1,76 @@
+"""Thin Python wrappers over the kernel-level C-ABI entry points (tests / profiling).
+
+Every wrapper takes torch CUDA tensors (PyTorch is plumbing: memory and streams) and
+passes raw pointers to libddit.so. Nothing here computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import Epi, check, lib, ptr, stream_ptr
+
+
+def _c(x) -> int | None:
+    return ptr(x) if isinstance(x, torch.Tensor) else x
+
+
+def gemm(
+    a: torch.Tensor,
+    w: torch.Tensor,
+    *,
+    epi: int = _lib.EPI_BF16,
+    bias: torch.Tensor | None = None,
+    out: torch.Tensor | None = None,
+    resid: torch.Tensor | None = None,
+    gate: torch.Tensor | None = None,
+    rows_per_b: int = 0,
+    out2: torch.Tensor | None = None,
+    qnorm_w: torch.Tensor | None = None,
+    knorm_w: torch.Tensor | None = None,
+    hidden: int = 0,
+    rope_tab: torch.Tensor | None = None,
+    rope_T: int = 1,
+    rope_S: int = 1,
+    eps: float = 1e-6,
+    bn: int = 128,
+    stream=None,
+) -> torch.Tensor | None:
+    """``epi(a @ w.T + bias)`` on tcgen05. a: [M,K] bf16, w: [N,K] bf16."""
+    assert a.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+    M, K = a.shape
+    N = w.shape[0]
+    assert w.shape[1] == K
+    if epi in (_lib.EPI_BF16, _lib.EPI_GELU_BF16, _lib.EPI_QKV) and out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=a.device)
+    if epi == _lib.EPI_F32 and out is None:
+        out = torch.empty(M, N, dtype=torch.float32, device=a.device)
+    e = Epi()
+    e.bias = _c(bias)
+    e.out = _c(out)
+    e.ldo = out.stride(0) if out is not None else 0
+    e.resid = _c(resid)
+    e.ldr = resid.stride(0) if resid is not None else 0
+    e.gate = _c(gate)
+    e.gate_stride = gate.stride(0) if gate is not None else 0
+    e.rows_per_b = rows_per_b
+    e.out2 = _c(out2)
+    e.ldo2 = out2.stride(0) if out2 is not None else 0
+    e.qnorm_w = _c(qnorm_w)
+    e.knorm_w = _c(knorm_w)
+    e.hidden = hidden
+    e.rope = 1 if rope_tab is not None else 0
+    e.rope_T = rope_T
+    e.rope_S = rope_S
+    e.rope_tab = _c(rope_tab)
+    e.eps = eps
+    check(
+        lib().ddit_gemm(
+            ptr(a), a.stride(0), ptr(w), w.stride(0), M, N, K, epi, ctypes.byref(e), bn,
+            stream_ptr(stream),
+        )
+    )
+    return out if epi != _lib.EPI_RESID else resid

@@ -1,0 +1,41 @@
+"""Time the STDiT3-XL/2 240p GEMM shapes on tcgen05 (ours) vs torch.matmul (cuBLAS)."""
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+from paper_2506_13497_b200 import _lib, kernels
+
+dev = torch.device("cuda:0")
+M = 2 * 6075
+shapes = [("qkv", 3456, 1152, 144, _lib.EPI_BF16), ("proj", 1152, 1152, 128, _lib.EPI_BF16),
+          ("fc1", 4608, 1152, 256, _lib.EPI_GELU_BF16), ("fc2", 1152, 4608, 128, _lib.EPI_BF16),
+          ("fc1_192", 4608, 1152, 192, _lib.EPI_GELU_BF16), ("proj192", 1152, 1152, 192, _lib.EPI_BF16),
+          ("big", 8192, 8192, 256, _lib.EPI_BF16)]
+for name, N, K, bn, epi in shapes:
+    m = M if name != "big" else 8192
+    a = torch.randn(m, K, device=dev).bfloat16()
+    w = (torch.randn(N, K, device=dev) / math.sqrt(K)).bfloat16()
+    bias = torch.zeros(N, device=dev)
+    out = torch.empty(m, N, device=dev, dtype=torch.bfloat16)
+    for _ in range(3):
+        kernels.gemm(a, w, epi=epi, bias=bias, out=out, bn=bn)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    it = 20
+    s.record()
+    for _ in range(it):
+        kernels.gemm(a, w, epi=epi, bias=bias, out=out, bn=bn)
+    e.record(); torch.cuda.synchronize()
+    t = s.elapsed_time(e) / it
+    for _ in range(3):
+        torch.matmul(a, w.T)
+    s.record()
+    for _ in range(it):
+        torch.matmul(a, w.T)
+    e.record(); torch.cuda.synchronize()
+    tc = s.elapsed_time(e) / it
+    fl = 2 * m * N * K
+    print(f"{name:8s} M={m} N={N} K={K} bn={bn}: ours {t*1e3:8.1f} us {fl/t/1e9:7.1f} TF/s | cublas {tc*1e3:8.1f} us {fl/tc/1e9:7.1f} TF/s", flush=True)

@@ -1,0 +1,98 @@
+"""tcgen05 GEMM + fused epilogues vs a plain torch fp32 reference of the same op."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a = a.float()
+    b = b.float()
+    return (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b).clamp_min(1e-30)).item()
+
+
+def _inputs(M, N, K, dev, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    a = torch.randn(M, K, generator=g).to(dev, torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) / math.sqrt(K)).to(dev, torch.bfloat16)
+    bias = (0.1 * torch.randn(N, generator=g)).to(dev)
+    return a, w, bias
+
+
+@pytest.mark.parametrize("bn", [128, 144, 192, 256])
+@pytest.mark.parametrize("M,N,K", [(128, 1152, 64), (300, 2304, 1152), (1000, 4608, 1152), (777, 1152, 4608)])
+def test_gemm_bias_bf16(cuda, bn, M, N, K):
+    from paper_2506_13497_b200 import kernels, _lib
+
+    if N % bn:
+        pytest.skip("N not a multiple of BN")
+    a, w, bias = _inputs(M, N, K, cuda)
+    out = kernels.gemm(a, w, epi=_lib.EPI_BF16, bias=bias, bn=bn)
+    ref = a.float() @ w.float().T + bias
+    torch.cuda.synchronize()
+    assert rel_l2(out, ref) < 5e-3
+
+
+def test_gemm_f32_and_gelu(cuda):
+    from paper_2506_13497_b200 import kernels, _lib
+
+    a, w, bias = _inputs(513, 4608, 1152, cuda, seed=1)
+    ref = a.float() @ w.float().T + bias
+    out = kernels.gemm(a, w, epi=_lib.EPI_F32, bias=bias, bn=256)
+    assert rel_l2(out, ref) < 1e-5
+    out = kernels.gemm(a, w, epi=_lib.EPI_GELU_BF16, bias=bias, bn=256)
+    assert rel_l2(out, torch.nn.functional.gelu(ref, approximate="tanh")) < 5e-3
+
+
+def test_gemm_resid_gate(cuda):
+    from paper_2506_13497_b200 import kernels, _lib
+
+    M, N, K = 2 * 607, 1152, 1152
+    a, w, bias = _inputs(M, N, K, cuda, seed=2)
+    x = torch.randn(M, N, device=cuda)
+    gate = torch.randn(2, N, device=cuda)
+    x0 = x.clone()
+    out2 = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, out2=out2, bn=128)
+    b = torch.arange(M, device=cuda) // (M // 2)
+    ref = x0 + gate[b] * (a.float() @ w.float().T + bias)
+    assert rel_l2(x, ref) < 1e-5
+    assert rel_l2(out2, ref) < 5e-3
+
+
+@pytest.mark.parametrize("rope", [False, True])
+def test_gemm_qkv_epilogue(cuda, rope):
+    from paper_2506_13497_b200 import kernels, _lib
+
+    C, H, D = 1152, 16, 72
+    T, S = 5, 37
+    M = 2 * T * S
+    a, w, bias = _inputs(M, 3 * C, C, cuda, seed=3)
+    qw = 1 + 0.1 * torch.randn(D, device=cuda)
+    kw = 1 + 0.1 * torch.randn(D, device=cuda)
+    freqs = 1.0 / (10000 ** (torch.arange(0, D, 2, dtype=torch.float64)[: D // 2] / D))
+    ang = torch.arange(T, dtype=torch.float64)[:, None] * freqs[None]
+    tab = torch.stack([ang.cos(), ang.sin()], -1).float().to(cuda).contiguous()
+    out = kernels.gemm(a, w, epi=_lib.EPI_QKV, bias=bias, qnorm_w=qw, knorm_w=kw, hidden=C,
+                       rope_tab=tab if rope else None, rope_T=T, rope_S=S, bn=144)
+    ref = (a.float() @ w.float().T + bias).view(M, 3, H, D)
+    q, k, v = ref.unbind(1)
+
+    def rms(x, wt):
+        return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-6) * wt
+
+    q, k = rms(q, qw), rms(k, kw)
+    if rope:
+        pos = (torch.arange(M, device=cuda) // S) % T
+        cs = tab[pos]  # [M, 36, 2]
+        def rot(x):
+            x2 = x.view(M, H, D // 2, 2)
+            c = cs[:, None, :, 0]
+            s = cs[:, None, :, 1]
+            a0, a1 = x2[..., 0], x2[..., 1]
+            return torch.stack([a0 * c - a1 * s, a1 * c + a0 * s], -1).view(M, H, D)
+        q, k = rot(q), rot(k)
+    ref = torch.stack([q, k, v], 1).view(M, 3 * C)
+    assert rel_l2(out, ref) < 5e-3
