@@ -75,6 +75,127 @@ typedef struct ddit_epi {
 DDIT_API int ddit_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                        int epi, const ddit_epi* ep, int bn, void* stream);
 
+/* Flash attention over bf16 q/k/v (head_dim 72). Token j of sequence i lives at row
+ *   (i / inner) * outer + (i % inner) * inner_stride + j * tok
+ * of the q (and o) matrix, and likewise with the kv_* map for k and v; head h occupies
+ * columns [72h, 72h+72). Covers spatial, temporal and cross attention without re-layout. */
+typedef struct ddit_attn {
+  const void* q; int ldq;
+  const void* k; int ldk;
+  const void* v; int ldv;
+  void* o; int ldo;
+  int heads;
+  int head_dim;
+  int num_seqs;
+  int Lq, Lk;
+  int q_inner, q_outer, q_inner_stride, q_tok;
+  int kv_inner, kv_outer, kv_inner_stride, kv_tok;
+  float scale;
+} ddit_attn;
+
+DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
+
+/* ------------------------------------------------------------------ the STDiT3 step
+ * Model = device weights (caller-owned, registered by pointer). Request = one video being
+ * denoised on one rank of a DoP-P group: shard geometry, workspace (caller-allocated), cached
+ * text embedding and per-block cross-attention K/V. The step replaces the reference's
+ * `ProfileTable.dit_step(res, dop)` lookup (profiles.py:69-76) at the engine's step sites
+ * (engine.py:245 start, :289 after a promotion, :292 steady state). */
+
+typedef struct ddit_config {
+  int depth;            /* 28 (spatial + temporal block pairs) */
+  int hidden;           /* C = 1152 */
+  int heads;            /* 16 */
+  int head_dim;         /* 72 */
+  int mlp_hidden;       /* 4608 */
+  int in_channels;      /* 4 */
+  int out_channels;     /* 8 (pred_sigma) */
+  int caption_channels; /* 4096 */
+  int text_tokens;      /* 300 */
+  int freq_dim;         /* 256 */
+  int input_sq_size;    /* 512 */
+  float eps;            /* 1e-6 */
+} ddit_config;
+
+/* Linear weights are bf16 [out, in] (nn.Linear layout); biases, tables and norms fp32. */
+typedef struct ddit_block_weights {
+  const float* scale_shift_table; /* [6, C] */
+  const void* qkv_w; const float* qkv_b;
+  const float* q_norm; const float* k_norm;
+  const void* proj_w; const float* proj_b;
+  const void* cq_w; const float* cq_b;
+  const void* ckv_w; const float* ckv_b;
+  const void* cproj_w; const float* cproj_b;
+  const void* fc1_w; const float* fc1_b;
+  const void* fc2_w; const float* fc2_b;
+} ddit_block_weights;
+
+typedef struct ddit_weights {
+  const float* x_emb_w;  /* fp32 [C, in*4] (Conv3d (1,2,2) flattened) */
+  const float* x_emb_b;
+  const void* t0_w; const float* t0_b; /* t_embedder.mlp.0: bf16 [C, 256] */
+  const void* t2_w; const float* t2_b; /* t_embedder.mlp.2: bf16 [C, C] */
+  const void* f0_w; const float* f0_b; /* fps_embedder.mlp.0 */
+  const void* f2_w; const float* f2_b; /* fps_embedder.mlp.2 */
+  const void* tb_w; const float* tb_b; /* t_block.1: bf16 [6C, C] */
+  const void* y1_w; const float* y1_b; /* y_embedder fc1: bf16 [C, 4096] */
+  const void* y2_w; const float* y2_b; /* y_embedder fc2: bf16 [C, C] */
+  const float* y_null;                 /* fp32 [300, 4096] */
+  const float* final_sst;              /* fp32 [2, C] */
+  const float* final_w;                /* fp32 [out*4, C] */
+  const float* final_b;                /* fp32 [out*4] */
+  const ddit_block_weights* blocks;    /* host array of 2*depth: spatial i at 2i, temporal 2i+1 */
+} ddit_weights;
+
+typedef struct ddit_req_desc {
+  int latent_t, latent_h, latent_w; /* z is [1, 4, T, Hl, Wl] */
+  int height, width;                /* pixels: pos-embed scale and timestep transform */
+  int dop, rank;                    /* DoP P in {1,2,4,8}; this rank */
+  int num_steps;                    /* 30 */
+  float guidance;                   /* 7.0 */
+  float fps;                        /* 24 */
+} ddit_req_desc;
+
+typedef struct ddit_model ddit_model;
+typedef struct ddit_req ddit_req;
+
+DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, ddit_model** out);
+DDIT_API void ddit_model_destroy(ddit_model* m);
+
+/* Bytes of device workspace a request needs (caller allocates, 256-byte aligned). */
+DDIT_API int ddit_request_workspace_bytes(const ddit_model* m, const ddit_req_desc* d,
+                                          uint64_t* bytes);
+/* Shard of this rank: frames [t_lo, t_hi) (spatial phase) and tokens [s_lo, s_hi) (temporal). */
+DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int* t_lo, int* t_hi,
+                                int* s_lo, int* s_hi);
+/* Opens a request: builds tables, embeds the caption y_cond (device fp32 [300, 4096]) together
+ * with the null caption, caches the per-block cross-attention K/V. */
+DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* workspace,
+                               uint64_t bytes, const float* y_cond, void* stream, ddit_req** out);
+DDIT_API void ddit_request_close(ddit_req* r);
+
+/* DoP > 1: register every rank's exchange buffers (x_sp, x_tp: fp32, as returned by
+ * ddit_request_exchange_buffers on that rank, peer-mapped) and flag arrays (uint32 [P]). */
+DDIT_API int ddit_request_exchange_buffers(ddit_req* r, void** x_sp, void** x_tp, void** flags);
+DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const* x_tp,
+                                    void* const* flags);
+
+/* One full denoise step on this rank. z_local: device fp32 [4][t_hi-t_lo][Hl][Wl], updated
+ * in place (z <- z + v * dt). For DoP > 1 every rank of the group calls it concurrently. */
+DDIT_API int ddit_dit_step(ddit_req* r, float* z_local, int step, void* stream);
+
+/* The same step split into phases (virtual ranks on one device drive these in lockstep):
+ * begin (t-embedding, modulation table, patch embed), phase k in [0, 2*depth) = block k
+ * followed by the push half of the exchange, end (final layer, CFG, Euler). */
+DDIT_API int ddit_step_begin(ddit_req* r, const float* z_local, int step, void* stream);
+DDIT_API int ddit_step_phase(ddit_req* r, int phase, void* stream);
+DDIT_API int ddit_step_end(ddit_req* r, float* z_local, int step, void* stream);
+/* Cross-rank barrier after a push (no-op at DoP 1). */
+DDIT_API int ddit_step_barrier(ddit_req* r, void* stream);
+
+/* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
+DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
+
 #ifdef __cplusplus
 }
 #endif

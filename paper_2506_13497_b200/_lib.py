@@ -39,6 +39,9 @@ class DditError(RuntimeError):
         self.code = code
 
 
+vp, ci, cf = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+
+
 class Epi(ctypes.Structure):
     _fields_ = [
         ("bias", ctypes.c_void_p),
@@ -60,6 +63,76 @@ class Epi(ctypes.Structure):
         ("rope_tab", ctypes.c_void_p),
         ("eps", ctypes.c_float),
     ]
+
+
+
+
+class CConfig(ctypes.Structure):
+    _fields_ = [
+        ("depth", ci), ("hidden", ci), ("heads", ci), ("head_dim", ci), ("mlp_hidden", ci),
+        ("in_channels", ci), ("out_channels", ci), ("caption_channels", ci),
+        ("text_tokens", ci), ("freq_dim", ci), ("input_sq_size", ci), ("eps", cf),
+    ]
+
+
+class CBlock(ctypes.Structure):
+    _fields_ = [
+        ("scale_shift_table", vp), ("qkv_w", vp), ("qkv_b", vp), ("q_norm", vp), ("k_norm", vp),
+        ("proj_w", vp), ("proj_b", vp), ("cq_w", vp), ("cq_b", vp), ("ckv_w", vp),
+        ("ckv_b", vp), ("cproj_w", vp), ("cproj_b", vp), ("fc1_w", vp), ("fc1_b", vp),
+        ("fc2_w", vp), ("fc2_b", vp),
+    ]
+
+
+class CWeights(ctypes.Structure):
+    _fields_ = [
+        ("x_emb_w", vp), ("x_emb_b", vp), ("t0_w", vp), ("t0_b", vp), ("t2_w", vp), ("t2_b", vp),
+        ("f0_w", vp), ("f0_b", vp), ("f2_w", vp), ("f2_b", vp), ("tb_w", vp), ("tb_b", vp),
+        ("y1_w", vp), ("y1_b", vp), ("y2_w", vp), ("y2_b", vp), ("y_null", vp),
+        ("final_sst", vp), ("final_w", vp), ("final_b", vp), ("blocks", ctypes.POINTER(CBlock)),
+    ]
+
+
+class CReqDesc(ctypes.Structure):
+    _fields_ = [
+        ("latent_t", ci), ("latent_h", ci), ("latent_w", ci), ("height", ci), ("width", ci),
+        ("dop", ci), ("rank", ci), ("num_steps", ci), ("guidance", cf), ("fps", cf),
+    ]
+
+
+class Attn(ctypes.Structure):
+    _fields_ = [
+        ("q", ctypes.c_void_p), ("ldq", ctypes.c_int),
+        ("k", ctypes.c_void_p), ("ldk", ctypes.c_int),
+        ("v", ctypes.c_void_p), ("ldv", ctypes.c_int),
+        ("o", ctypes.c_void_p), ("ldo", ctypes.c_int),
+        ("heads", ctypes.c_int), ("head_dim", ctypes.c_int), ("num_seqs", ctypes.c_int),
+        ("Lq", ctypes.c_int), ("Lk", ctypes.c_int),
+        ("q_inner", ctypes.c_int), ("q_outer", ctypes.c_int), ("q_inner_stride", ctypes.c_int),
+        ("q_tok", ctypes.c_int),
+        ("kv_inner", ctypes.c_int), ("kv_outer", ctypes.c_int), ("kv_inner_stride", ctypes.c_int),
+        ("kv_tok", ctypes.c_int),
+        ("scale", ctypes.c_float),
+    ]
+
+
+_SIGNATURES = {
+    "ddit_attention": [ctypes.POINTER(Attn), vp],
+    "ddit_model_create": [ctypes.POINTER(CConfig), ctypes.POINTER(CWeights), ctypes.POINTER(vp)],
+    "ddit_request_workspace_bytes": [vp, ctypes.POINTER(CReqDesc), ctypes.POINTER(ctypes.c_uint64)],
+    "ddit_request_shard": [vp, ctypes.POINTER(CReqDesc)] + [ctypes.POINTER(ci)] * 4,
+    "ddit_request_open": [vp, ctypes.POINTER(CReqDesc), vp, ctypes.c_uint64, vp, vp,
+                          ctypes.POINTER(vp)],
+    "ddit_request_exchange_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
+    "ddit_request_set_peers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
+    "ddit_dit_step": [vp, vp, ci, vp],
+    "ddit_step_begin": [vp, vp, ci, vp],
+    "ddit_step_phase": [vp, ci, vp],
+    "ddit_step_end": [vp, vp, ci, vp],
+    "ddit_step_barrier": [vp, vp],
+    "ddit_request_timestep": [vp, ci, ctypes.POINTER(cf), ctypes.POINTER(cf)],
+}
+_VOID_FUNCS = {"ddit_model_destroy": [vp], "ddit_request_close": [vp]}
 
 
 _lib = None
@@ -88,15 +161,19 @@ def _declare(h: ctypes.CDLL) -> None:
     h.ddit_num_sms.restype = ci
     h.ddit_gemm.restype = ci
     h.ddit_gemm.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, ctypes.POINTER(Epi), ci, vp]
-    for name, argtypes in _EXTRA_SIGNATURES.items():
+    for name, argtypes in _SIGNATURES.items():
         fn = getattr(h, name)
         fn.restype = ci
         fn.argtypes = argtypes
+    for name, argtypes in _VOID_FUNCS.items():
+        fn = getattr(h, name)
+        fn.restype = None
+        fn.argtypes = argtypes
 
 
-# Filled in by the modules that bind further entry points (kept in one table so the
-# symbol-export test can check every declared function).
-_EXTRA_SIGNATURES: dict[str, list] = {}
+def exported_entry_points() -> list[str]:
+    """Every C-ABI function this binding declares (the symbol-export test checks them)."""
+    return ["ddit_last_error", "ddit_version", "ddit_num_sms", "ddit_gemm", *_SIGNATURES, *_VOID_FUNCS]
 
 
 def check(rc: int) -> None:

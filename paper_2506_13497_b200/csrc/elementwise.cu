@@ -1,0 +1,350 @@
+// Memory-bound kernels of the STDiT3 step: fused
+// LayerNorm + t2i-modulate, timestep / fps embedding GEMVs, the per-step modulation table of
+// all blocks, patch-embed + pos-embed (step entry), and the fused exit (final LayerNorm +
+// modulate + Linear + unpatchify + CFG combine + rectified-flow Euler update).
+#include "common.cuh"
+#include "elementwise.cuh"
+
+namespace ddit {
+
+// ------------------------------------------------------------------ LN + modulate (K1)
+// xm[r, :] = bf16( LN(x[r, :]) * (1 + scale[b]) + shift[b] ),  b = r / rows_per_b.
+// One warp per row; C % 4 == 0 and C <= 32 * 4 * kMaxVec.
+static constexpr int kMaxVec = 12;  // C up to 1536
+
+__global__ void __launch_bounds__(256)
+    ln_modulate_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int M, int C,
+                       const float* __restrict__ shift, const float* __restrict__ scale,
+                       int mod_stride, int rows_per_b, float eps) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * C);
+  const int nv = C >> 2;
+  float4 v[kMaxVec];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      v[i] = __ldg(xr + c);
+      s += v[i].x + v[i].y + v[i].z + v[i].w;
+    }
+  }
+  const float mean = warp_sum(s) / C;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      q += a * a + b * b + cc * cc + d * d;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / C + eps);
+  const int bidx = row / rows_per_b;
+  const float4* sh = reinterpret_cast<const float4*>(shift + (size_t)bidx * mod_stride);
+  const float4* sc = reinterpret_cast<const float4*>(scale + (size_t)bidx * mod_stride);
+  uint2* o = reinterpret_cast<uint2*>(out + (size_t)row * C);
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nv) {
+      const float4 a = __ldg(sh + c), k = __ldg(sc + c);
+      const float y0 = (v[i].x - mean) * rstd * (1.f + k.x) + a.x;
+      const float y1 = (v[i].y - mean) * rstd * (1.f + k.y) + a.y;
+      const float y2 = (v[i].z - mean) * rstd * (1.f + k.z) + a.z;
+      const float y3 = (v[i].w - mean) * rstd * (1.f + k.w) + a.w;
+      o[c] = make_uint2(pack_bf16(y0, y1), pack_bf16(y2, y3));
+    }
+  }
+}
+
+int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
+                const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s) {
+  if (C % 4 || C > 32 * 4 * kMaxVec || M <= 0) return -2;
+  ln_modulate_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, out, M, C, shift, scale, mod_stride,
+                                                  rows_per_b > 0 ? rows_per_b : M, eps);
+  return 0;
+}
+
+// ------------------------------------------------------------------ t / fps embedding (K10)
+// freq[j, :] = [cos(t_j * f), sin(t_j * f)], f_i = exp(-ln(10000) i / half), for the B
+// timesteps followed by the B fps values.
+__global__ void timestep_freq_kernel(float* __restrict__ freq, const float* __restrict__ tvals,
+                                     int nvals, int dim) {
+  const int j = blockIdx.x;
+  const int half = dim / 2;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float f = expf(-9.210340371976184f * (float)i / (float)half);  // ln(10000)
+    const float a = tvals[j] * f;
+    freq[j * dim + i] = cosf(a);
+    freq[j * dim + half + i] = sinf(a);
+  }
+}
+
+// y[b, n] (+)= W[n, :] . act(x[b, :]) + bias[n] ; W bf16 [N, K]; one warp per output n.
+// in_act: 0 none, 1 SiLU. out_act: 0 none, 1 SiLU. accumulate: add to y instead of store.
+__global__ void __launch_bounds__(256)
+    gemv_kernel(const __nv_bfloat16* __restrict__ W, const float* __restrict__ bias,
+                const float* __restrict__ x, float* __restrict__ y, int nb, int N, int K,
+                int in_act, int out_act, int accumulate) {
+  const int n = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const __nv_bfloat16* w = W + (size_t)n * K;
+  for (int k = lane * 8; k < K; k += 32 * 8) {
+    const uint4 wv = *reinterpret_cast<const uint4*>(w + k);
+    const uint32_t wr[4] = {wv.x, wv.y, wv.z, wv.w};
+    float wf[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = unpack_bf16(wr[e]);
+      wf[2 * e] = f.x;
+      wf[2 * e + 1] = f.y;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (b >= nb) break;
+      const float* xb = x + (size_t)b * K + k;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float xv = xb[e];
+        if (in_act == 1) xv = silu(xv);
+        acc[b] += wf[e] * xv;
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (b >= nb) break;
+    float r = warp_sum(acc[b]);
+    if (lane == 0) {
+      r += bias ? bias[n] : 0.f;
+      if (out_act == 1) r = silu(r);
+      float* dst = y + (size_t)b * N + n;
+      *dst = accumulate ? *dst + r : r;
+    }
+  }
+}
+
+int gemv(const __nv_bfloat16* W, const float* bias, const float* x, float* y, int nb, int N, int K,
+         int in_act, int out_act, int accumulate, cudaStream_t s) {
+  if (nb > 4 || K % 8) return -2;
+  gemv_kernel<<<(N + 7) / 8, 256, 0, s>>>(W, bias, x, y, nb, N, K, in_act, out_act, accumulate);
+  return 0;
+}
+
+int timestep_freq(float* freq, const float* tvals, int nvals, int dim, cudaStream_t s) {
+  timestep_freq_kernel<<<nvals, 128, 0, s>>>(freq, tvals, nvals, dim);
+  return 0;
+}
+
+// mods[blk][b][6C] = sst[blk][6C] + t_mlp[b][6C]   for blk < nblocks
+// fin[b][2C]      = fsst[2C] + t[b][C] (broadcast over the 2 rows)
+__global__ void modulation_kernel(float* __restrict__ mods, const float* const* __restrict__ sst,
+                                  const float* __restrict__ t_mlp, int nblocks, int nb, int C6,
+                                  float* __restrict__ fin, const float* __restrict__ fsst,
+                                  const float* __restrict__ t, int C) {
+  const int blk = blockIdx.y;
+  if (blk < nblocks) {
+    const float* table = sst[blk];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb * C6; i += gridDim.x * blockDim.x) {
+      const int b = i / C6, j = i % C6;
+      mods[((size_t)blk * nb + b) * C6 + j] = table[j] + t_mlp[(size_t)b * C6 + j];
+    }
+  } else {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb * 2 * C; i += gridDim.x * blockDim.x) {
+      const int b = i / (2 * C), j = i % (2 * C);
+      fin[i] = fsst[j] + t[(size_t)b * C + (j % C)];
+    }
+  }
+}
+
+int modulation(float* mods, const float* const* sst, const float* t_mlp, int nblocks, int nb,
+               int C, float* fin, const float* fsst, const float* t, cudaStream_t s) {
+  dim3 grid(8, nblocks + 1);
+  modulation_kernel<<<grid, 256, 0, s>>>(mods, sst, t_mlp, nblocks, nb, 6 * C, fin, fsst, t, C);
+  return 0;
+}
+
+// ------------------------------------------------------------------ tables
+// pos[s][C]: OpenSora PositionEmbedding2D -- first half encodes the column coordinate,
+// second half the row coordinate; each half = [sin(p f), cos(p f)], f_i = 10000^(-2i/(C/2)).
+__global__ void pos_embed_kernel(float* __restrict__ pos, int h, int w, int C, float scale,
+                                 float base_size) {
+  const int s = blockIdx.x;
+  const int i = s / w, j = s % w;
+  const float prow = (float)i / scale * (base_size / (float)h);
+  const float pcol = (float)j / scale * (base_size / (float)w);
+  const int half = C / 2, q = C / 4;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int part = c / half;  // 0: column coordinate, 1: row coordinate
+    const int r = c % half;
+    const int fi = r % q;
+    const float f = 1.0f / powf(10000.0f, (float)(2 * fi) / (float)half);
+    const float p = (part == 0 ? pcol : prow) * f;
+    pos[(size_t)s * C + c] = r < q ? sinf(p) : cosf(p);
+  }
+}
+
+// rope[t][i] = (cos(t th_i), sin(t th_i)), th_i = 10000^(-2i/D)
+__global__ void rope_table_kernel(float2* __restrict__ tab, int T, int D) {
+  const int t = blockIdx.x;
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const double th = 1.0 / pow(10000.0, (double)(2 * i) / (double)D);
+    const double a = (double)t * th;
+    tab[t * (D / 2) + i] = make_float2((float)cos(a), (float)sin(a));
+  }
+}
+
+int build_tables(float* pos, int h, int w, int C, float scale, float base_size, float* rope, int T,
+                 int D, cudaStream_t s) {
+  pos_embed_kernel<<<h * w, 128, 0, s>>>(pos, h, w, C, scale, base_size);
+  rope_table_kernel<<<T, 64, 0, s>>>(reinterpret_cast<float2*>(rope), T, D);
+  return 0;
+}
+
+// ------------------------------------------------------------------ step entry (K9)
+// x[b][t][s][c] = bias[c] + sum_{ci,dh,dw} Wp[c][ci][dh][dw] z[ci][t][2i+dh][2j+dw] + pos[s][c]
+// z: the local T-shard [Cin][Tl][Hl][Wl] fp32 (zero outside Hl x Wl); same x for all nb copies.
+__global__ void __launch_bounds__(256)
+    patch_embed_kernel(const float* __restrict__ z, const float* __restrict__ Wp,
+                       const float* __restrict__ bp, const float* __restrict__ pos,
+                       float* __restrict__ x, int Tl, int Hl, int Wl, int h, int w, int C,
+                       int Cin, int nb) {
+  const int tok = blockIdx.x;  // t * S + s
+  const int S = h * w;
+  const int t = tok / S, s = tok % S;
+  const int i = s / w, j = s % w;
+  __shared__ float patch[64];
+  if (threadIdx.x < Cin * 4) {
+    const int ci = threadIdx.x / 4, dh = (threadIdx.x / 2) % 2, dw = threadIdx.x % 2;
+    const int y = 2 * i + dh, xx = 2 * j + dw;
+    patch[threadIdx.x] =
+        (y < Hl && xx < Wl) ? z[(((size_t)ci * Tl + t) * Hl + y) * Wl + xx] : 0.f;
+  }
+  __syncthreads();
+  const int K = Cin * 4;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = bp[c] + pos[(size_t)s * C + c];
+    const float* wr = Wp + (size_t)c * K;
+    for (int k = 0; k < K; ++k) acc += wr[k] * patch[k];
+    for (int b = 0; b < nb; ++b) x[((size_t)b * Tl * S + tok) * C + c] = acc;
+  }
+}
+
+int patch_embed(const float* z, const float* Wp, const float* bp, const float* pos, float* x, int Tl,
+                int Hl, int Wl, int h, int w, int C, int Cin, int nb, cudaStream_t s) {
+  if (Tl <= 0) return 0;
+  patch_embed_kernel<<<Tl * h * w, 256, 0, s>>>(z, Wp, bp, pos, x, Tl, Hl, Wl, h, w, C, Cin, nb);
+  return 0;
+}
+
+// ------------------------------------------------------------------ step exit (K9)
+// For each local token (t, s) and both CFG halves b = 0 (cond), 1 (uncond):
+//   y_b = LN(x_b) * (1 + scale_b) + shift_b ;  o_b[f] = Wf[f] . y_b + bf[f]
+// for the 16 features f = (hp*2 + wp)*out_ch + c with c < Cin (the sigma half is unused);
+//   v = o_uncond + g (o_cond - o_uncond);  z[c][t][2i+hp][2j+wp] += v * dt.
+__global__ void __launch_bounds__(128)
+    final_layer_kernel(const float* __restrict__ x, const float* __restrict__ fin,
+                       const float* __restrict__ Wf, const float* __restrict__ bf,
+                       float* __restrict__ z, int Tl, int Hl, int Wl, int h, int w, int C,
+                       int Cin, int out_ch, float guidance, float dt, float eps) {
+  const int tok = blockIdx.x;
+  const int S = h * w;
+  const int t = tok / S, s = tok % S;
+  const int i = s / w, j = s % w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ float red[2][4][2];
+  __shared__ float stats[2][2];
+  __shared__ float outv[2][16];
+  // LayerNorm stats for the two CFG rows
+  for (int b = 0; b < 2; ++b) {
+    const float* xr = x + ((size_t)b * Tl * S + tok) * C;
+    float sm = 0.f, sq = 0.f;
+    for (int c = threadIdx.x; c < C; c += 128) {
+      const float v = xr[c];
+      sm += v;
+      sq += v * v;
+    }
+    sm = warp_sum(sm);
+    sq = warp_sum(sq);
+    if (lane == 0) {
+      red[b][warp][0] = sm;
+      red[b][warp][1] = sq;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int b = threadIdx.x;
+    float sm = 0.f, sq = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      sm += red[b][k][0];
+      sq += red[b][k][1];
+    }
+    const float mean = sm / C;
+    const float var = fmaxf(sq / C - mean * mean, 0.f);
+    stats[b][0] = mean;
+    stats[b][1] = rsqrtf(var + eps);
+  }
+  __syncthreads();
+  // 32 dot products (16 features x 2 rows); warp w takes features 4w..4w+3
+  for (int fi = 0; fi < 4; ++fi) {
+    const int f16 = warp * 4 + fi;           // (hp*2+wp)*Cin + c
+    const int pidx = f16 / Cin, c = f16 % Cin;
+    const int feat = pidx * out_ch + c;
+    const float* wr = Wf + (size_t)feat * C;
+    for (int b = 0; b < 2; ++b) {
+      const float* xr = x + ((size_t)b * Tl * S + tok) * C;
+      const float* sh = fin + (size_t)b * 2 * C;
+      const float* sc = sh + C;
+      float acc = 0.f;
+      for (int cc = lane; cc < C; cc += 32) {
+        const float yv = (xr[cc] - stats[b][0]) * stats[b][1] * (1.f + sc[cc]) + sh[cc];
+        acc += wr[cc] * yv;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) outv[b][f16] = acc + bf[feat];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 * Cin) {
+    const int f16 = threadIdx.x;
+    const int pidx = f16 / Cin, c = f16 % Cin;
+    const int hp = pidx / 2, wp = pidx % 2;
+    const int yy = 2 * i + hp, xx = 2 * j + wp;
+    if (yy < Hl && xx < Wl) {
+      const float v = outv[1][f16] + guidance * (outv[0][f16] - outv[1][f16]);
+      float* zp = z + (((size_t)c * Tl + t) * Hl + yy) * Wl + xx;
+      *zp = *zp + v * dt;
+    }
+  }
+}
+
+int final_layer(const float* x, const float* fin, const float* Wf, const float* bf, float* z, int Tl,
+                int Hl, int Wl, int h, int w, int C, int Cin, int out_ch, float guidance, float dt,
+                float eps, cudaStream_t s) {
+  if (Tl <= 0) return 0;
+  if (4 * Cin > 16) return -2;
+  final_layer_kernel<<<Tl * h * w, 128, 0, s>>>(x, fin, Wf, bf, z, Tl, Hl, Wl, h, w, C, Cin, out_ch,
+                                                 guidance, dt, eps);
+  return 0;
+}
+
+// ------------------------------------------------------------------ misc
+__global__ void cast_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                 size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16(in[i]);
+}
+
+int cast_bf16(const float* in, __nv_bfloat16* out, size_t n, cudaStream_t s) {
+  const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  cast_bf16_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(in, out, n);
+  return 0;
+}
+
+}  // namespace ddit

@@ -8,7 +8,7 @@
 // The accumulator is double-buffered in TMEM so the epilogue of tile i overlaps the MMAs of
 // tile i+1. Tiles are distributed round-robin over a grid of min(#tiles, #SMs) CTAs.
 // Shapes in the DDiT step: M = tokens (ragged, TMA zero-fills the
-// tail), K in {1152, 4096, 4608}, N in {1152, 2304, 3456, 4608}; N % BN == 0 and K % 64 == 0.
+// tail, and the K tail), K in {1152, 4096, 4608}, N in {1152, 2304, 3456, 4608}; N % BN == 0.
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = N / BN;
   const int num_tiles = m_tiles * n_tiles;
-  const int k_blocks = K / BK;
+  const int k_blocks = (K + BK - 1) / BK;  // TMA zero-fills the K tail
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -386,7 +386,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
     snprintf(g_err, sizeof g_err, "unsupported BN %d", bn);
     return -2;
   }
-  if (M <= 0 || N % bn != 0 || K % BK != 0 || K <= 0) {
+  if (M <= 0 || N % bn != 0 || K <= 0) {
     snprintf(g_err, sizeof g_err, "bad GEMM shape M=%d N=%d K=%d BN=%d", M, N, K, bn);
     return -2;
   }

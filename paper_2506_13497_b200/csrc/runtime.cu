@@ -1,0 +1,631 @@
+// STDiT3 step runtime behind the C ABI: model registration, request (shard geometry,
+// workspace carve-up, text / cross-attention K/V cache, pre-built GEMM plans) and the
+// denoise step as a fixed kernel sequence on one stream (capturable in a CUDA graph).
+//
+// Step (rank r of a DoP-P group):
+//   begin : t / fps embedding -> t_block -> modulation table of all 2*depth blocks (+ final);
+//           patch-embed + pos-embed of the local frames into x_sp [B][Tl][S][C] (fp32)
+//   phase : for each block k: LN+mod -> QKV GEMM (+bias, q/k RMSNorm, RoPE) -> self-attn ->
+//           proj GEMM (+gate, residual, bf16 copy) -> cross-q GEMM -> cross-attn -> out GEMM
+//           (+residual) -> LN+mod -> fc1 GEMM (+GELU) -> fc2 GEMM (+gate, residual);
+//           then (P > 1) push x to the other layout on every rank (sp->tp after spatial
+//           blocks, tp->sp after temporal blocks) and barrier
+//   end   : final LN+mod + Linear + unpatchify + CFG + Euler on the local frames of z
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "capi_internal.h"
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "exchange.cuh"
+#include "gemm_sm100.cuh"
+
+namespace ddit {
+int attention_launch(const ddit_attn* a, cudaStream_t s);
+}
+
+using namespace ddit;
+typedef __nv_bfloat16 bf16;
+
+struct ddit_model {
+  ddit_config cfg;
+  ddit_weights w;
+  std::vector<ddit_block_weights> blocks;
+  const float** sst_dev = nullptr;  // device array of 2*depth scale_shift_table pointers
+};
+
+namespace {
+enum { G_QKV = 0, G_PROJ, G_CQ, G_CPROJ, G_FC1, G_FC2, G_N };
+
+struct Geometry {
+  int B = 2;
+  int T, Hl, Wl, h, w, S;
+  int P, rank;
+  int t_lo, t_hi, s_lo, s_hi, Tl, Sl;
+  int M_sp, M_tp, Mmax;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Carve {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  }
+};
+
+struct Layout {
+  size_t x_sp, x_tp, xb, xm, big, ao, mods, fin, temb, tmlp, hbuf, freq, tv, pos, rope, yemb, kv,
+      flags, total;
+};
+
+int geometry(const ddit_config& c, const ddit_req_desc& d, Geometry* g) {
+  if (d.dop < 1 || d.dop > kMaxDop || (d.dop & (d.dop - 1)) || d.rank < 0 || d.rank >= d.dop) {
+    set_error("dop %d / rank %d invalid (dop must be a power of two <= %d)", d.dop, d.rank,
+              kMaxDop);
+    return DDIT_E_LOOKUP;
+  }
+  if (d.latent_t <= 0 || d.latent_h <= 0 || d.latent_w <= 0 || d.num_steps <= 0) {
+    set_error("bad request shape");
+    return DDIT_E_INVALID;
+  }
+  g->T = d.latent_t;
+  g->Hl = d.latent_h;
+  g->Wl = d.latent_w;
+  g->h = (d.latent_h + 1) / 2;
+  g->w = (d.latent_w + 1) / 2;
+  g->S = g->h * g->w;
+  g->P = d.dop;
+  g->rank = d.rank;
+  const int tc = (g->T + g->P - 1) / g->P, sc = (g->S + g->P - 1) / g->P;
+  g->t_lo = std::min(d.rank * tc, g->T);
+  g->t_hi = std::min((d.rank + 1) * tc, g->T);
+  g->s_lo = std::min(d.rank * sc, g->S);
+  g->s_hi = std::min((d.rank + 1) * sc, g->S);
+  g->Tl = g->t_hi - g->t_lo;
+  g->Sl = g->s_hi - g->s_lo;
+  g->M_sp = g->B * g->Tl * g->S;
+  g->M_tp = g->B * g->T * g->Sl;
+  g->Mmax = std::max(g->M_sp, g->M_tp);
+  (void)c;
+  return DDIT_OK;
+}
+
+Layout layout(const ddit_config& c, const Geometry& g) {
+  Layout L;
+  Carve cv;
+  const size_t C = c.hidden;
+  const size_t Ly = (size_t)g.B * c.text_tokens;
+  const size_t nblk = 2 * (size_t)c.depth;
+  L.x_sp = cv.take((size_t)std::max(g.M_sp, 1) * C * 4);
+  L.x_tp = g.P > 1 ? cv.take((size_t)std::max(g.M_tp, 1) * C * 4) : L.x_sp;
+  L.xb = cv.take((size_t)g.Mmax * C * 2);
+  L.xm = cv.take((size_t)g.Mmax * C * 2);
+  size_t big = std::max((size_t)g.Mmax * std::max((size_t)c.mlp_hidden, 3 * C),
+                        Ly * (size_t)c.caption_channels + Ly * C);
+  L.big = cv.take(big * 2);
+  L.ao = cv.take((size_t)g.Mmax * C * 2);
+  L.mods = cv.take(nblk * g.B * 6 * C * 4);
+  L.fin = cv.take((size_t)g.B * 2 * C * 4);
+  L.temb = cv.take((size_t)g.B * C * 4);
+  L.tmlp = cv.take((size_t)g.B * 6 * C * 4);
+  L.hbuf = cv.take((size_t)g.B * C * 4);
+  L.freq = cv.take((size_t)2 * g.B * c.freq_dim * 4);
+  L.tv = cv.take(4096 * 4);
+  L.pos = cv.take((size_t)g.S * C * 4);
+  L.rope = cv.take((size_t)g.T * c.head_dim * 4);
+  L.yemb = cv.take(Ly * C * 2);
+  L.kv = cv.take(nblk * Ly * 2 * C * 2);
+  L.flags = cv.take(kMaxDop * 4);
+  L.total = cv.off;
+  return L;
+}
+
+}  // namespace
+
+struct ddit_req {
+  ddit_model* m;
+  ddit_req_desc d;
+  Geometry g;
+  Layout L;
+  uint8_t* ws;
+  float *x_sp, *x_tp, *mods, *fin, *temb, *tmlp, *hbuf, *freq, *tv, *pos, *rope;
+  bf16 *xb, *xm, *big, *ao, *yemb, *kv;
+  uint32_t* flags;
+  std::vector<float> ts;  // transformed timesteps
+  std::vector<GemmPlan> plans;  // [2*depth][G_N]
+  PeerPtrs peer_sp{}, peer_tp{};
+  PeerFlags peer_flags{};
+  bool peers_set = false;
+  uint32_t epoch = 0;
+};
+
+namespace {
+
+// RFLOW timesteps with the OpenSora-1.2 resolution/length transform (oracle/stdit3.py).
+std::vector<float> rflow_timesteps(const ddit_req_desc& d) {
+  std::vector<float> out(d.num_steps);
+  const double ratio = std::sqrt((double)d.height * d.width / (512.0 * 512.0)) *
+                       std::sqrt((double)d.latent_t);
+  for (int i = 0; i < d.num_steps; ++i) {
+    const double u = 1.0 - (double)i / d.num_steps;
+    out[i] = (float)(ratio * u / (1.0 + (ratio - 1.0) * u) * 1000.0);
+  }
+  return out;
+}
+
+float step_dt(const ddit_req* r, int step) {
+  const auto& ts = r->ts;
+  const double dt = step < (int)ts.size() - 1 ? (double)ts[step] - ts[step + 1] : ts[step];
+  return (float)(dt / 1000.0);
+}
+
+int build_plans(ddit_req* r) {
+  const ddit_config& c = r->m->cfg;
+  const Geometry& g = r->g;
+  const int C = c.hidden;
+  const int nblk = 2 * c.depth;
+  r->plans.assign((size_t)nblk * G_N, GemmPlan{});
+  const int bn_c = (C % 192 == 0) ? 192 : ((C % 144 == 0) ? 144 : 128);
+  const int bn_mlp = (c.mlp_hidden % 256 == 0) ? 256 : ((c.mlp_hidden % 192 == 0) ? 192 : 144);
+  for (int k = 0; k < nblk; ++k) {
+    const bool temporal = k & 1;
+    const int M = temporal ? g.M_tp : g.M_sp;
+    if (M == 0) continue;
+    float* x = temporal ? r->x_tp : r->x_sp;
+    const int rpb = M / g.B;
+    const ddit_block_weights& bw = r->m->blocks[k];
+    const float* mod = r->mods + (size_t)k * g.B * 6 * C;
+    GemmPlan* P = &r->plans[(size_t)k * G_N];
+    EpiParams e;
+    int rc;
+    // QKV: bias + q/k RMSNorm (+ RoPE over frames for temporal blocks)
+    memset(&e, 0, sizeof e);
+    e.bias = bw.qkv_b;
+    e.out = r->big;
+    e.ldo = 3 * C;
+    e.qnorm_w = bw.q_norm;
+    e.knorm_w = bw.k_norm;
+    e.hidden = C;
+    e.rope = temporal ? 1 : 0;
+    e.rope_T = g.T;
+    e.rope_S = temporal ? g.Sl : g.S;
+    e.rope_tab = reinterpret_cast<const float2*>(r->rope);
+    e.eps = c.eps;
+    e.rows_per_b = rpb;
+    if ((rc = gemm_plan_init(&P[G_QKV], r->xm, C, bw.qkv_w, C, M, 3 * C, C, EPI_QKV, e, 144)))
+      return rc;
+    // attention out-projection: x += gate_msa * (.) ; bf16 copy of x for cross-attn queries
+    memset(&e, 0, sizeof e);
+    e.bias = bw.proj_b;
+    e.resid = x;
+    e.ldr = C;
+    e.gate = mod + 2 * C;
+    e.gate_stride = 6 * C;
+    e.rows_per_b = rpb;
+    e.out2 = r->xb;
+    e.ldo2 = C;
+    if ((rc = gemm_plan_init(&P[G_PROJ], r->ao, C, bw.proj_w, C, M, C, C, EPI_RESID, e, bn_c)))
+      return rc;
+    // cross-attn queries
+    memset(&e, 0, sizeof e);
+    e.bias = bw.cq_b;
+    e.out = r->xm;
+    e.ldo = C;
+    e.rows_per_b = rpb;
+    if ((rc = gemm_plan_init(&P[G_CQ], r->xb, C, bw.cq_w, C, M, C, C, EPI_BF16, e, bn_c))) return rc;
+    // cross-attn out projection: x += (.)
+    memset(&e, 0, sizeof e);
+    e.bias = bw.cproj_b;
+    e.resid = x;
+    e.ldr = C;
+    e.rows_per_b = rpb;
+    if ((rc = gemm_plan_init(&P[G_CPROJ], r->ao, C, bw.cproj_w, C, M, C, C, EPI_RESID, e, bn_c)))
+      return rc;
+    // MLP
+    memset(&e, 0, sizeof e);
+    e.bias = bw.fc1_b;
+    e.out = r->big;
+    e.ldo = c.mlp_hidden;
+    e.rows_per_b = rpb;
+    if ((rc = gemm_plan_init(&P[G_FC1], r->xm, C, bw.fc1_w, C, M, c.mlp_hidden, C, EPI_GELU_BF16, e,
+                             bn_mlp)))
+      return rc;
+    memset(&e, 0, sizeof e);
+    e.bias = bw.fc2_b;
+    e.resid = x;
+    e.ldr = C;
+    e.gate = mod + 5 * C;
+    e.gate_stride = 6 * C;
+    e.rows_per_b = rpb;
+    if ((rc = gemm_plan_init(&P[G_FC2], r->big, c.mlp_hidden, bw.fc2_w, c.mlp_hidden, M, C,
+                             c.mlp_hidden, EPI_RESID, e, bn_c)))
+      return rc;
+  }
+  return DDIT_OK;
+}
+
+int launch(const GemmPlan& p, cudaStream_t s) {
+  int rc = gemm_plan_launch(&p, s);
+  if (rc) {
+    set_error("gemm: %s", gemm_last_error());
+    return DDIT_E_CUDA;
+  }
+  return DDIT_OK;
+}
+
+int run_block(ddit_req* r, int k, cudaStream_t s) {
+  const ddit_config& c = r->m->cfg;
+  const Geometry& g = r->g;
+  const int C = c.hidden;
+  const bool temporal = k & 1;
+  const int M = temporal ? g.M_tp : g.M_sp;
+  if (M == 0) return DDIT_OK;
+  const int rpb = M / g.B;
+  float* x = temporal ? r->x_tp : r->x_sp;
+  const float* mod = r->mods + (size_t)k * g.B * 6 * C;
+  const GemmPlan* P = &r->plans[(size_t)k * G_N];
+  int rc;
+  if (ln_modulate(x, r->xm, M, C, mod + 0 * C, mod + 1 * C, 6 * C, rpb, c.eps, s)) {
+    set_error("ln_modulate: bad shape");
+    return DDIT_E_INVALID;
+  }
+  if ((rc = launch(P[G_QKV], s))) return rc;
+  ddit_attn a;
+  memset(&a, 0, sizeof a);
+  a.q = r->big;
+  a.k = r->big + C;
+  a.v = r->big + 2 * C;
+  a.ldq = a.ldk = a.ldv = 3 * C;
+  a.o = r->ao;
+  a.ldo = C;
+  a.heads = c.heads;
+  a.head_dim = c.head_dim;
+  a.scale = 1.0f / std::sqrt((float)c.head_dim);
+  if (!temporal) {  // frames are the sequences: [B*Tl] x S
+    a.num_seqs = g.B * g.Tl;
+    a.Lq = a.Lk = g.S;
+    a.q_inner = a.kv_inner = 1;
+    a.q_outer = a.kv_outer = g.S;
+    a.q_tok = a.kv_tok = 1;
+  } else {  // token positions are the sequences: [B*Sl] x T, stride Sl
+    a.num_seqs = g.B * g.Sl;
+    a.Lq = a.Lk = g.T;
+    a.q_inner = a.kv_inner = g.Sl;
+    a.q_outer = a.kv_outer = g.T * g.Sl;
+    a.q_inner_stride = a.kv_inner_stride = 1;
+    a.q_tok = a.kv_tok = g.Sl;
+  }
+  if ((rc = attention_launch(&a, s))) return rc;
+  if ((rc = launch(P[G_PROJ], s))) return rc;
+  if ((rc = launch(P[G_CQ], s))) return rc;
+  // cross attention: each batch's rows attend to its own 300 text tokens
+  const bf16* kv = r->kv + (size_t)k * g.B * c.text_tokens * 2 * C;
+  memset(&a, 0, sizeof a);
+  a.q = r->xm;
+  a.ldq = C;
+  a.k = kv;
+  a.v = kv + C;
+  a.ldk = a.ldv = 2 * C;
+  a.o = r->ao;
+  a.ldo = C;
+  a.heads = c.heads;
+  a.head_dim = c.head_dim;
+  a.num_seqs = g.B;
+  a.Lq = rpb;
+  a.Lk = c.text_tokens;
+  a.q_inner = a.kv_inner = 1;
+  a.q_outer = rpb;
+  a.kv_outer = c.text_tokens;
+  a.q_tok = a.kv_tok = 1;
+  a.scale = 1.0f / std::sqrt((float)c.head_dim);
+  if ((rc = attention_launch(&a, s))) return rc;
+  if ((rc = launch(P[G_CPROJ], s))) return rc;
+  if (ln_modulate(x, r->xm, M, C, mod + 3 * C, mod + 4 * C, 6 * C, rpb, c.eps, s)) {
+    set_error("ln_modulate: bad shape");
+    return DDIT_E_INVALID;
+  }
+  if ((rc = launch(P[G_FC1], s))) return rc;
+  if ((rc = launch(P[G_FC2], s))) return rc;
+  return DDIT_OK;
+}
+
+int push_exchange(ddit_req* r, int k, cudaStream_t s) {
+  const Geometry& g = r->g;
+  if (g.P == 1) return DDIT_OK;
+  if (!r->peers_set) {
+    set_error("DoP %d request has no peers registered", g.P);
+    return DDIT_E_CONFIG;
+  }
+  const int C = r->m->cfg.hidden;
+  if ((k & 1) == 0)
+    exchange_sp_to_tp(r->x_sp, r->peer_tp, g.B, g.T, g.S, C, g.P, g.t_lo, g.Tl, s);
+  else
+    exchange_tp_to_sp(r->x_tp, r->peer_sp, g.B, g.T, g.S, C, g.P, g.s_lo, g.Sl, s);
+  return check_cuda("exchange");
+}
+
+}  // namespace
+
+extern "C" {
+
+DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, ddit_model** out) {
+  if (!cfg || !w || !out || !w->blocks) {
+    set_error("ddit_model_create: null argument");
+    return DDIT_E_INVALID;
+  }
+  if (cfg->head_dim != 72 || cfg->heads * cfg->head_dim != cfg->hidden ||
+      cfg->hidden % 144 != 0 || cfg->in_channels * 4 > 16) {
+    set_error("ddit_model_create: unsupported config (head_dim 72, C %% 144 == 0 required)");
+    return DDIT_E_CONFIG;
+  }
+  ddit_model* m = new (std::nothrow) ddit_model();
+  if (!m) return DDIT_E_ALLOC;
+  m->cfg = *cfg;
+  m->w = *w;
+  m->blocks.assign(w->blocks, w->blocks + 2 * cfg->depth);
+  m->w.blocks = nullptr;
+  std::vector<const float*> sst(2 * cfg->depth);
+  for (int k = 0; k < 2 * cfg->depth; ++k) sst[k] = m->blocks[k].scale_shift_table;
+  if (cudaMalloc(&m->sst_dev, sst.size() * sizeof(float*)) != cudaSuccess ||
+      cudaMemcpy(m->sst_dev, sst.data(), sst.size() * sizeof(float*), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    set_error("ddit_model_create: cudaMalloc failed");
+    delete m;
+    return DDIT_E_ALLOC;
+  }
+  *out = m;
+  return DDIT_OK;
+}
+
+DDIT_API void ddit_model_destroy(ddit_model* m) {
+  if (!m) return;
+  cudaFree(m->sst_dev);
+  delete m;
+}
+
+DDIT_API int ddit_request_workspace_bytes(const ddit_model* m, const ddit_req_desc* d,
+                                          uint64_t* bytes) {
+  Geometry g;
+  int rc = geometry(m->cfg, *d, &g);
+  if (rc) return rc;
+  *bytes = layout(m->cfg, g).total;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int* t_lo, int* t_hi,
+                                int* s_lo, int* s_hi) {
+  Geometry g;
+  int rc = geometry(m->cfg, *d, &g);
+  if (rc) return rc;
+  *t_lo = g.t_lo;
+  *t_hi = g.t_hi;
+  *s_lo = g.s_lo;
+  *s_hi = g.s_hi;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* workspace,
+                               uint64_t bytes, const float* y_cond, void* stream, ddit_req** out) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ddit_req* r = new (std::nothrow) ddit_req();
+  if (!r) return DDIT_E_ALLOC;
+  r->m = m;
+  r->d = *d;
+  int rc = geometry(m->cfg, *d, &r->g);
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  r->L = layout(m->cfg, r->g);
+  if (bytes < r->L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
+    set_error("workspace too small or misaligned (%llu < %llu)", (unsigned long long)bytes,
+              (unsigned long long)r->L.total);
+    delete r;
+    return DDIT_E_ALLOC;
+  }
+  const ddit_config& c = m->cfg;
+  const Geometry& g = r->g;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  r->ws = ws;
+  r->x_sp = reinterpret_cast<float*>(ws + r->L.x_sp);
+  r->x_tp = reinterpret_cast<float*>(ws + r->L.x_tp);
+  r->xb = reinterpret_cast<bf16*>(ws + r->L.xb);
+  r->xm = reinterpret_cast<bf16*>(ws + r->L.xm);
+  r->big = reinterpret_cast<bf16*>(ws + r->L.big);
+  r->ao = reinterpret_cast<bf16*>(ws + r->L.ao);
+  r->mods = reinterpret_cast<float*>(ws + r->L.mods);
+  r->fin = reinterpret_cast<float*>(ws + r->L.fin);
+  r->temb = reinterpret_cast<float*>(ws + r->L.temb);
+  r->tmlp = reinterpret_cast<float*>(ws + r->L.tmlp);
+  r->hbuf = reinterpret_cast<float*>(ws + r->L.hbuf);
+  r->freq = reinterpret_cast<float*>(ws + r->L.freq);
+  r->tv = reinterpret_cast<float*>(ws + r->L.tv);
+  r->pos = reinterpret_cast<float*>(ws + r->L.pos);
+  r->rope = reinterpret_cast<float*>(ws + r->L.rope);
+  r->yemb = reinterpret_cast<bf16*>(ws + r->L.yemb);
+  r->kv = reinterpret_cast<bf16*>(ws + r->L.kv);
+  r->flags = reinterpret_cast<uint32_t*>(ws + r->L.flags);
+  r->ts = rflow_timesteps(*d);
+  if (d->num_steps > 1000) {
+    set_error("num_steps too large");
+    delete r;
+    return DDIT_E_INVALID;
+  }
+  // timestep table tv[step][4] = {t, t, fps, fps}
+  std::vector<float> tv((size_t)d->num_steps * 4);
+  for (int i = 0; i < d->num_steps; ++i) {
+    tv[4 * i + 0] = tv[4 * i + 1] = r->ts[i];
+    tv[4 * i + 2] = tv[4 * i + 3] = d->fps;
+  }
+  cudaMemcpyAsync(r->tv, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(r->flags, 0, kMaxDop * 4, s);
+  // tables
+  const int base_size = (int)std::lround(std::sqrt((double)g.S));
+  const float scale = (float)(std::sqrt((double)d->height * d->width) / c.input_sq_size);
+  build_tables(r->pos, g.h, g.w, c.hidden, scale, (float)base_size, r->rope, g.T, c.head_dim, s);
+  // text: [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb [B*300, C]
+  const int Ly = g.B * c.text_tokens;
+  const size_t ycount = (size_t)c.text_tokens * c.caption_channels;
+  bf16* ycat = r->big;
+  bf16* yhid = r->big + (size_t)Ly * c.caption_channels;
+  cast_bf16(y_cond, ycat, ycount, s);
+  cast_bf16(m->w.y_null, ycat + ycount, ycount, s);
+  GemmPlan gp;
+  EpiParams e;
+  memset(&e, 0, sizeof e);
+  e.bias = m->w.y1_b;
+  e.out = yhid;
+  e.ldo = c.hidden;
+  if ((rc = gemm_plan_init(&gp, ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly,
+                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, 144)) ||
+      (rc = launch(gp, s))) {
+    set_error("y_embedder fc1: %s", gemm_last_error());
+    delete r;
+    return DDIT_E_CUDA;
+  }
+  e.bias = m->w.y2_b;
+  e.out = r->yemb;
+  if ((rc = gemm_plan_init(&gp, yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden,
+                           EPI_BF16, e, 144)) ||
+      (rc = launch(gp, s))) {
+    set_error("y_embedder fc2: %s", gemm_last_error());
+    delete r;
+    return DDIT_E_CUDA;
+  }
+  // per-block cross-attention K/V cache: kv[k] = yemb . Wkv^T + b  [B*300, 2C]
+  for (int k = 0; k < 2 * c.depth; ++k) {
+    memset(&e, 0, sizeof e);
+    e.bias = m->blocks[k].ckv_b;
+    e.out = r->kv + (size_t)k * Ly * 2 * c.hidden;
+    e.ldo = 2 * c.hidden;
+    if ((rc = gemm_plan_init(&gp, r->yemb, c.hidden, m->blocks[k].ckv_w, c.hidden, Ly,
+                             2 * c.hidden, c.hidden, EPI_BF16, e, 144)) ||
+        (rc = launch(gp, s))) {
+      set_error("cross kv: %s", gemm_last_error());
+      delete r;
+      return DDIT_E_CUDA;
+    }
+  }
+  if ((rc = build_plans(r))) {
+    set_error("plan: %s", gemm_last_error());
+    delete r;
+    return rc == -3 ? DDIT_E_TMA : DDIT_E_INVALID;
+  }
+  if ((rc = check_cuda("ddit_request_open"))) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return DDIT_OK;
+}
+
+DDIT_API void ddit_request_close(ddit_req* r) { delete r; }
+
+DDIT_API int ddit_request_exchange_buffers(ddit_req* r, void** x_sp, void** x_tp, void** flags) {
+  *x_sp = r->x_sp;
+  *x_tp = r->x_tp;
+  *flags = r->flags;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const* x_tp,
+                                    void* const* flags) {
+  for (int q = 0; q < r->g.P; ++q) {
+    r->peer_sp.p[q] = static_cast<float*>(x_sp[q]);
+    r->peer_tp.p[q] = static_cast<float*>(x_tp[q]);
+    r->peer_flags.p[q] = flags ? static_cast<uint32_t*>(flags[q]) : nullptr;
+  }
+  r->peers_set = true;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt) {
+  if (step < 0 || step >= r->d.num_steps) {
+    set_error("step %d outside [0, %d)", step, r->d.num_steps);
+    return DDIT_E_INVALID;
+  }
+  *t = r->ts[step];
+  *dt = step_dt(r, step);
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_step_begin(ddit_req* r, const float* z_local, int step, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (step < 0 || step >= r->d.num_steps) {
+    set_error("step %d outside [0, %d)", step, r->d.num_steps);
+    return DDIT_E_INVALID;
+  }
+  const ddit_model* m = r->m;
+  const ddit_config& c = m->cfg;
+  const ddit_weights& w = m->w;
+  const Geometry& g = r->g;
+  const int C = c.hidden, B = g.B;
+  // t / fps embedding -> t (temb) -> t_block (tmlp)
+  timestep_freq(r->freq, r->tv + 4 * step, 2 * B, c.freq_dim, s);
+  const float* ft = r->freq;
+  const float* ff = r->freq + (size_t)B * c.freq_dim;
+  gemv(static_cast<const bf16*>(w.t0_w), w.t0_b, ft, r->hbuf, B, C, c.freq_dim, 0, 1, 0, s);
+  gemv(static_cast<const bf16*>(w.t2_w), w.t2_b, r->hbuf, r->temb, B, C, C, 0, 0, 0, s);
+  gemv(static_cast<const bf16*>(w.f0_w), w.f0_b, ff, r->hbuf, B, C, c.freq_dim, 0, 1, 0, s);
+  gemv(static_cast<const bf16*>(w.f2_w), w.f2_b, r->hbuf, r->temb, B, C, C, 0, 0, 1, s);
+  gemv(static_cast<const bf16*>(w.tb_w), w.tb_b, r->temb, r->tmlp, B, 6 * C, C, 1, 0, 0, s);
+  modulation(r->mods, m->sst_dev, r->tmlp, 2 * c.depth, B, C, r->fin, w.final_sst, r->temb, s);
+  patch_embed(z_local, w.x_emb_w, w.x_emb_b, r->pos, r->x_sp, g.Tl, g.Hl, g.Wl, g.h, g.w, C,
+              c.in_channels, B, s);
+  return check_cuda("ddit_step_begin");
+}
+
+DDIT_API int ddit_step_phase(ddit_req* r, int phase, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (phase < 0 || phase >= 2 * r->m->cfg.depth) {
+    set_error("phase %d out of range", phase);
+    return DDIT_E_INVALID;
+  }
+  int rc = run_block(r, phase, s);
+  if (rc) return rc;
+  if ((rc = check_cuda("block"))) return rc;
+  return push_exchange(r, phase, s);
+}
+
+DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
+  if (r->g.P == 1) return DDIT_OK;
+  if (!r->peers_set || !r->peer_flags.p[0]) {
+    set_error("barrier: flags of the group not registered");
+    return DDIT_E_CONFIG;
+  }
+  r->epoch += 1;
+  flag_barrier(r->peer_flags, r->g.rank, r->g.P, r->epoch, static_cast<cudaStream_t>(stream));
+  return check_cuda("barrier");
+}
+
+DDIT_API int ddit_step_end(ddit_req* r, float* z_local, int step, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ddit_model* m = r->m;
+  const ddit_config& c = m->cfg;
+  const Geometry& g = r->g;
+  if (final_layer(r->x_sp, r->fin, m->w.final_w, m->w.final_b, z_local, g.Tl, g.Hl, g.Wl, g.h, g.w,
+                  c.hidden, c.in_channels, c.out_channels, r->d.guidance, step_dt(r, step), c.eps,
+                  s)) {
+    set_error("final layer: unsupported channel count");
+    return DDIT_E_CONFIG;
+  }
+  return check_cuda("ddit_step_end");
+}
+
+DDIT_API int ddit_dit_step(ddit_req* r, float* z_local, int step, void* stream) {
+  int rc = ddit_step_begin(r, z_local, step, stream);
+  if (rc) return rc;
+  for (int k = 0; k < 2 * r->m->cfg.depth; ++k) {
+    if ((rc = ddit_step_phase(r, k, stream))) return rc;
+    if ((rc = ddit_step_barrier(r, stream))) return rc;
+  }
+  return ddit_step_end(r, z_local, step, stream);
+}
+
+}  // extern "C"

@@ -11,7 +11,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import Epi, check, lib, ptr, stream_ptr
+from ._lib import Attn, Epi, check, lib, ptr, stream_ptr
 
 
 def _c(x) -> int | None:
@@ -74,3 +74,19 @@ def gemm(
         )
     )
     return out if epi != _lib.EPI_RESID else resid
+
+
+def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
+              q_map=(1, 0, 0, 1), kv_map=(1, 0, 0, 1), scale: float | None = None, stream=None):
+    """Flash attention over token-major bf16 matrices; maps = (inner, outer, inner_stride, tok)."""
+    a = Attn()
+    a.q, a.ldq = ptr(q), q.stride(0)
+    a.k, a.ldk = ptr(k), k.stride(0)
+    a.v, a.ldv = ptr(v), v.stride(0)
+    a.o, a.ldo = ptr(o), o.stride(0)
+    a.heads, a.head_dim, a.num_seqs, a.Lq, a.Lk = heads, 72, num_seqs, Lq, Lk
+    a.q_inner, a.q_outer, a.q_inner_stride, a.q_tok = q_map
+    a.kv_inner, a.kv_outer, a.kv_inner_stride, a.kv_tok = kv_map
+    a.scale = scale if scale is not None else 72 ** -0.5
+    check(lib().ddit_attention(ctypes.byref(a), stream_ptr(stream)))
+    return o

@@ -1,0 +1,62 @@
+"""Flash attention (spatial / temporal / cross index maps) vs torch fp32 softmax attention."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+H, D = 16, 72
+
+
+def rel_l2(a, b):
+    return (torch.linalg.vector_norm(a.float() - b.float()) / torch.linalg.vector_norm(b.float())).item()
+
+
+def ref_attn(q, k, v):  # [n, L, H, D]
+    s = torch.einsum("nqhd,nkhd->nhqk", q.float(), k.float()) * D**-0.5
+    return torch.einsum("nhqk,nkhd->nqhd", s.softmax(-1), v.float())
+
+
+@pytest.mark.parametrize("B,T,S", [(2, 3, 405), (2, 1, 64), (1, 2, 130), (2, 4, 1)])
+def test_spatial(cuda, B, T, S):
+    from paper_2506_13497_b200 import kernels
+    g = torch.Generator().manual_seed(0)
+    M = B * T * S
+    qkv = torch.randn(M, 3 * H * D, generator=g).to(cuda, torch.bfloat16)
+    o = torch.zeros(M, H * D, device=cuda, dtype=torch.bfloat16)
+    C = H * D
+    kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=H, num_seqs=B * T,
+                      Lq=S, Lk=S, q_map=(1, S, 0, 1), kv_map=(1, S, 0, 1))
+    q, k, v = qkv.view(B * T, S, 3, H, D).unbind(2)
+    ref = ref_attn(q, k, v).reshape(M, C)
+    assert rel_l2(o, ref) < 1e-2
+
+
+@pytest.mark.parametrize("B,T,Sl", [(2, 15, 405), (2, 30, 17), (1, 4, 3), (2, 70, 5)])
+def test_temporal(cuda, B, T, Sl):
+    from paper_2506_13497_b200 import kernels
+    g = torch.Generator().manual_seed(1)
+    M = B * T * Sl
+    C = H * D
+    qkv = torch.randn(M, 3 * C, generator=g).to(cuda, torch.bfloat16)
+    o = torch.zeros(M, C, device=cuda, dtype=torch.bfloat16)
+    mp = (Sl, T * Sl, 1, Sl)
+    kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=H, num_seqs=B * Sl,
+                      Lq=T, Lk=T, q_map=mp, kv_map=mp)
+    x = qkv.view(B, T, Sl, 3, H, D).transpose(1, 2).reshape(B * Sl, T, 3, H, D)
+    q, k, v = x.unbind(2)
+    ref = ref_attn(q, k, v).reshape(B, Sl, T, C).transpose(1, 2).reshape(M, C)
+    assert rel_l2(o, ref) < 1e-2
+
+
+@pytest.mark.parametrize("B,N,Ly", [(2, 777, 300), (2, 64, 300), (1, 100, 17)])
+def test_cross(cuda, B, N, Ly):
+    from paper_2506_13497_b200 import kernels
+    g = torch.Generator().manual_seed(2)
+    C = H * D
+    q = torch.randn(B * N, C, generator=g).to(cuda, torch.bfloat16)
+    kv = torch.randn(B * Ly, 2 * C, generator=g).to(cuda, torch.bfloat16)
+    o = torch.zeros(B * N, C, device=cuda, dtype=torch.bfloat16)
+    kernels.attention(q, kv[:, :C], kv[:, C:], o, heads=H, num_seqs=B, Lq=N, Lk=Ly,
+                      q_map=(1, N, 0, 1), kv_map=(1, Ly, 0, 1))
+    kk, vv = kv.view(B, Ly, 2, H, D).unbind(2)
+    ref = ref_attn(q.view(B, N, H, D), kk, vv).reshape(B * N, C)
+    assert rel_l2(o, ref) < 1e-2
