@@ -196,6 +196,22 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream);
 /* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
 
+/* Profiling: while enabled every launch of the request is bracketed by CUDA events on its
+ * stream; _read returns per-class totals (ms, launches) for classes
+ * 0 = tcgen05 GEMM, 1 = attention, 2 = elementwise / embed / final, 3 = exchange + barrier,
+ * and resets. */
+DDIT_API int ddit_request_profile(ddit_req* r, int enable);
+DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count);
+/* Total kernel launches issued by libddit in this process. */
+DDIT_API unsigned long long ddit_launch_count(void);
+
+/* ------------------------------------------------------------------ cross-process mapping
+ * One process per GPU: a rank exports the (allocation handle, offset) of its exchange buffers
+ * and the group's other ranks map them (peer access over NVLink). handle = 64 bytes. */
+DDIT_API int ddit_ipc_export(const void* ptr, void* handle, uint64_t* offset);
+DDIT_API int ddit_ipc_import(const void* handle, uint64_t offset, void** ptr);
+DDIT_API int ddit_ipc_close(void* ptr, uint64_t offset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -131,6 +131,11 @@ _SIGNATURES = {
     "ddit_step_end": [vp, vp, ci, vp],
     "ddit_step_barrier": [vp, vp],
     "ddit_request_timestep": [vp, ci, ctypes.POINTER(cf), ctypes.POINTER(cf)],
+    "ddit_request_profile": [vp, ci],
+    "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
+    "ddit_ipc_export": [vp, vp, ctypes.POINTER(ctypes.c_uint64)],
+    "ddit_ipc_import": [vp, ctypes.c_uint64, ctypes.POINTER(vp)],
+    "ddit_ipc_close": [vp, ctypes.c_uint64],
 }
 _VOID_FUNCS = {"ddit_model_destroy": [vp], "ddit_request_close": [vp]}
 
@@ -161,6 +166,8 @@ def _declare(h: ctypes.CDLL) -> None:
     h.ddit_num_sms.restype = ci
     h.ddit_gemm.restype = ci
     h.ddit_gemm.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, ctypes.POINTER(Epi), ci, vp]
+    h.ddit_launch_count.restype = ctypes.c_ulonglong
+    h.ddit_launch_count.argtypes = []
     for name, argtypes in _SIGNATURES.items():
         fn = getattr(h, name)
         fn.restype = ci
@@ -173,7 +180,8 @@ def _declare(h: ctypes.CDLL) -> None:
 
 def exported_entry_points() -> list[str]:
     """Every C-ABI function this binding declares (the symbol-export test checks them)."""
-    return ["ddit_last_error", "ddit_version", "ddit_num_sms", "ddit_gemm", *_SIGNATURES, *_VOID_FUNCS]
+    return ["ddit_last_error", "ddit_version", "ddit_num_sms", "ddit_gemm", "ddit_launch_count",
+            *_SIGNATURES, *_VOID_FUNCS]
 
 
 def check(rc: int) -> None:

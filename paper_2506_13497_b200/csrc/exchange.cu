@@ -5,15 +5,41 @@
 //
 //   x_sp of rank r: [B][Tl_r][S][C]      (frames t_lo_r .. t_lo_r + Tl_r - 1, all tokens)
 //   x_tp of rank q: [B][T][Sl_q][C]      (all frames, tokens s_lo_q .. s_lo_q + Sl_q - 1)
-// One warp moves one token row (C fp32) with 16-byte vectors.
+// One warp moves one token row (C fp32) with 16-byte vectors. When flags are registered the
+// last CTA to finish (ticket counter) publishes `epoch` into every peer's flag slot for this
+// rank after a system-scope fence, so a peer that observes the flag also observes the rows.
 #include "common.cuh"
 #include "exchange.cuh"
 
 namespace ddit {
 
+DDIT_DEV void signal_peers(const ExchangeSync& sync) {
+  // called by one thread of the last CTA
+  __threadfence_system();
+  for (int q = 0; q < sync.P; ++q) {
+    uint32_t* remote = sync.flags.p[q] + sync.rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(sync.epoch) : "memory");
+  }
+}
+
+DDIT_DEV void finish_cta(const ExchangeSync& sync) {
+  if (sync.flags.p[0] == nullptr) return;
+  __syncthreads();
+  __shared__ unsigned int ticket;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    ticket = atomicAdd(sync.counter, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ticket == gridDim.x - 1) {
+    *sync.counter = 0;  // reset for the next exchange (stream-ordered)
+    signal_peers(sync);
+  }
+}
+
 __global__ void __launch_bounds__(256)
     exchange_sp_to_tp_kernel(const float* __restrict__ src, PeerPtrs dst, int B, int T, int S,
-                             int C, int P, int t_lo, int Tl, int s_chunk) {
+                             int C, int t_lo, int Tl, int s_chunk, ExchangeSync sync) {
   const int rows = B * Tl * S;
   const int nv = C >> 2;
   for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
@@ -29,11 +55,12 @@ __global__ void __launch_bounds__(256)
                                            (((size_t)b * T + t_lo + tl) * Sl + (s - s_lo)) * C);
     for (int i = threadIdx.x & 31; i < nv; i += 32) dp[i] = __ldg(sp + i);
   }
+  finish_cta(sync);
 }
 
 __global__ void __launch_bounds__(256)
     exchange_tp_to_sp_kernel(const float* __restrict__ src, PeerPtrs dst, int B, int T, int S,
-                             int C, int P, int s_lo, int Sl, int t_chunk) {
+                             int C, int s_lo, int Sl, int t_chunk, ExchangeSync sync) {
   const int rows = B * T * Sl;
   const int nv = C >> 2;
   for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < rows; row += gridDim.x * 8) {
@@ -49,49 +76,49 @@ __global__ void __launch_bounds__(256)
                                            (((size_t)b * Tlq + (t - t_lo)) * S + s_lo + sl) * C);
     for (int i = threadIdx.x & 31; i < nv; i += 32) dp[i] = __ldg(sp + i);
   }
+  finish_cta(sync);
+}
+
+static int grid_for(int rows) {
+  int grid = (rows + 7) / 8;
+  if (grid > 4 * 148) grid = 4 * 148;
+  return grid < 1 ? 1 : grid;
 }
 
 int exchange_sp_to_tp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
-                      int t_lo, int Tl, cudaStream_t s) {
+                      int t_lo, int Tl, const ExchangeSync& sync, cudaStream_t s) {
   const int rows = B * Tl * S;
-  if (rows <= 0) return 0;
+  if (rows <= 0 && sync.flags.p[0] == nullptr) return 0;
   const int s_chunk = (S + P - 1) / P;
-  int grid = (rows + 7) / 8;
-  if (grid > 4 * 148) grid = 4 * 148;
-  exchange_sp_to_tp_kernel<<<grid, 256, 0, s>>>(src, dst, B, T, S, C, P, t_lo, Tl, s_chunk);
-  return 0;
+  exchange_sp_to_tp_kernel<<<grid_for(rows), 256, 0, s>>>(src, dst, B, T, S, C, t_lo, Tl, s_chunk,
+                                                          sync);
+  return 1;
 }
 
 int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
-                      int s_lo, int Sl, cudaStream_t s) {
+                      int s_lo, int Sl, const ExchangeSync& sync, cudaStream_t s) {
   const int rows = B * T * Sl;
-  if (rows <= 0) return 0;
+  if (rows <= 0 && sync.flags.p[0] == nullptr) return 0;
   const int t_chunk = (T + P - 1) / P;
-  int grid = (rows + 7) / 8;
-  if (grid > 4 * 148) grid = 4 * 148;
-  exchange_tp_to_sp_kernel<<<grid, 256, 0, s>>>(src, dst, B, T, S, C, P, s_lo, Sl, t_chunk);
-  return 0;
+  exchange_tp_to_sp_kernel<<<grid_for(rows), 256, 0, s>>>(src, dst, B, T, S, C, s_lo, Sl, t_chunk,
+                                                          sync);
+  return 1;
 }
 
-// Flag barrier: thread q publishes `epoch` into rank q's flag slot for this rank, then every
-// thread waits until its own slot from rank q reached `epoch`. Flags live in memory visible to
-// all ranks (peer-mapped); system-scope release/acquire orders the pushed rows.
-__global__ void flag_barrier_kernel(PeerFlags flags, int rank, int P, uint32_t epoch) {
+// Wait until every rank q published `epoch` into this rank's slot q.
+__global__ void flag_wait_kernel(const uint32_t* flags, int P, uint32_t epoch) {
   const int q = threadIdx.x;
   if (q >= P) return;
-  __threadfence_system();
-  volatile uint32_t* remote = flags.p[q] + rank;
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");
-  volatile uint32_t* mine = flags.p[rank] + q;
+  const uint32_t* mine = flags + q;
   uint32_t v;
   do {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
   } while ((int32_t)(v - epoch) < 0);
 }
 
-int flag_barrier(const PeerFlags& flags, int rank, int P, uint32_t epoch, cudaStream_t s) {
-  flag_barrier_kernel<<<1, 32, 0, s>>>(flags, rank, P, epoch);
-  return 0;
+int flag_wait(const uint32_t* own_flags, int P, uint32_t epoch, cudaStream_t s) {
+  flag_wait_kernel<<<1, 32, 0, s>>>(own_flags, P, epoch);
+  return 1;
 }
 
 }  // namespace ddit

@@ -11,9 +11,18 @@ struct PeerPtrs {
 struct PeerFlags {
   uint32_t* p[kMaxDop];
 };
+// Completion signalling of one exchange: flags.p[q] = rank q's flag array (uint32 [P]),
+// counter = this rank's CTA ticket counter (device, zero-initialised).
+struct ExchangeSync {
+  PeerFlags flags;  // p[0] == nullptr: no signalling (virtual ranks, stream-ordered)
+  unsigned int* counter;
+  int rank, P;
+  uint32_t epoch;
+};
+// Return the number of kernels launched (0 or 1).
 int exchange_sp_to_tp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
-                      int t_lo, int Tl, cudaStream_t s);
+                      int t_lo, int Tl, const ExchangeSync& sync, cudaStream_t s);
 int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
-                      int s_lo, int Sl, cudaStream_t s);
-int flag_barrier(const PeerFlags& flags, int rank, int P, uint32_t epoch, cudaStream_t s);
+                      int s_lo, int Sl, const ExchangeSync& sync, cudaStream_t s);
+int flag_wait(const uint32_t* own_flags, int P, uint32_t epoch, cudaStream_t s);
 }  // namespace ddit

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <new>
 #include <vector>
 
@@ -61,7 +62,7 @@ struct Carve {
 
 struct Layout {
   size_t x_sp, x_tp, xb, xm, big, ao, mods, fin, temb, tmlp, hbuf, freq, tv, pos, rope, yemb, kv,
-      flags, total;
+      flags, counter, total;
 };
 
 int geometry(const ddit_config& c, const ddit_req_desc& d, Geometry* g) {
@@ -122,6 +123,7 @@ Layout layout(const ddit_config& c, const Geometry& g) {
   L.yemb = cv.take(Ly * C * 2);
   L.kv = cv.take(nblk * Ly * 2 * C * 2);
   L.flags = cv.take(kMaxDop * 4);
+  L.counter = cv.take(16);
   L.total = cv.off;
   return L;
 }
@@ -137,13 +139,55 @@ struct ddit_req {
   float *x_sp, *x_tp, *mods, *fin, *temb, *tmlp, *hbuf, *freq, *tv, *pos, *rope;
   bf16 *xb, *xm, *big, *ao, *yemb, *kv;
   uint32_t* flags;
+  unsigned int* counter;
   std::vector<float> ts;  // transformed timesteps
   std::vector<GemmPlan> plans;  // [2*depth][G_N]
   PeerPtrs peer_sp{}, peer_tp{};
   PeerFlags peer_flags{};
   bool peers_set = false;
+  bool flags_set = false;
   uint32_t epoch = 0;
+  // profiling: event pairs around every launch, tagged by kernel class
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_cls;
+  size_t ev_n = 0;
+  ~ddit_req() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
 };
+
+static std::atomic<unsigned long long> g_launches{0};
+
+namespace {
+enum { K_GEMM = 0, K_ATTN = 1, K_EW = 2, K_EXCH = 3, K_NCLASS = 4 };
+
+// Run `f` (which launches kernels on s and returns 0 / a DDIT_E code) counting `n` launches
+// and, when profiling, bracketing it with a pair of events of class `cls`.
+template <class F>
+int timed(ddit_req* r, int cls, cudaStream_t s, int n, F&& f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (r->prof_on) {
+    while (r->ev.size() < 2 * (r->ev_n + 1)) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) break;
+      r->ev.push_back(e);
+    }
+    if (r->ev.size() >= 2 * (r->ev_n + 1)) {
+      e0 = r->ev[2 * r->ev_n];
+      e1 = r->ev[2 * r->ev_n + 1];
+      if (r->ev_cls.size() <= r->ev_n) r->ev_cls.resize(r->ev_n + 1);
+      r->ev_cls[r->ev_n] = cls;
+      r->ev_n++;
+      cudaEventRecord(e0, s);
+    }
+  }
+  int rc = f();
+  if (e1) cudaEventRecord(e1, s);
+  g_launches += (unsigned long long)n;
+  return rc;
+}
+}  // namespace
 
 namespace {
 
@@ -259,6 +303,24 @@ int launch(const GemmPlan& p, cudaStream_t s) {
   return DDIT_OK;
 }
 
+int launch_g(ddit_req* r, const GemmPlan& p, cudaStream_t s) {
+  return timed(r, K_GEMM, s, 1, [&] { return launch(p, s); });
+}
+int ln_mod(ddit_req* r, float* x, int M, const float* shift, const float* scale, int rpb,
+           cudaStream_t s) {
+  const ddit_config& c = r->m->cfg;
+  return timed(r, K_EW, s, 1, [&] {
+    if (ln_modulate(x, r->xm, M, c.hidden, shift, scale, 6 * c.hidden, rpb, c.eps, s)) {
+      set_error("ln_modulate: bad shape");
+      return (int)DDIT_E_INVALID;
+    }
+    return (int)DDIT_OK;
+  });
+}
+int attn(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
+  return timed(r, K_ATTN, s, 1, [&] { return attention_launch(a, s); });
+}
+
 int run_block(ddit_req* r, int k, cudaStream_t s) {
   const ddit_config& c = r->m->cfg;
   const Geometry& g = r->g;
@@ -271,11 +333,8 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
   const float* mod = r->mods + (size_t)k * g.B * 6 * C;
   const GemmPlan* P = &r->plans[(size_t)k * G_N];
   int rc;
-  if (ln_modulate(x, r->xm, M, C, mod + 0 * C, mod + 1 * C, 6 * C, rpb, c.eps, s)) {
-    set_error("ln_modulate: bad shape");
-    return DDIT_E_INVALID;
-  }
-  if ((rc = launch(P[G_QKV], s))) return rc;
+  if ((rc = ln_mod(r, x, M, mod + 0 * C, mod + 1 * C, rpb, s))) return rc;
+  if ((rc = launch_g(r, P[G_QKV], s))) return rc;
   ddit_attn a;
   memset(&a, 0, sizeof a);
   a.q = r->big;
@@ -301,9 +360,9 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
     a.q_inner_stride = a.kv_inner_stride = 1;
     a.q_tok = a.kv_tok = g.Sl;
   }
-  if ((rc = attention_launch(&a, s))) return rc;
-  if ((rc = launch(P[G_PROJ], s))) return rc;
-  if ((rc = launch(P[G_CQ], s))) return rc;
+  if ((rc = attn(r, &a, s))) return rc;
+  if ((rc = launch_g(r, P[G_PROJ], s))) return rc;
+  if ((rc = launch_g(r, P[G_CQ], s))) return rc;
   // cross attention: each batch's rows attend to its own 300 text tokens
   const bf16* kv = r->kv + (size_t)k * g.B * c.text_tokens * 2 * C;
   memset(&a, 0, sizeof a);
@@ -324,14 +383,11 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
   a.kv_outer = c.text_tokens;
   a.q_tok = a.kv_tok = 1;
   a.scale = 1.0f / std::sqrt((float)c.head_dim);
-  if ((rc = attention_launch(&a, s))) return rc;
-  if ((rc = launch(P[G_CPROJ], s))) return rc;
-  if (ln_modulate(x, r->xm, M, C, mod + 3 * C, mod + 4 * C, 6 * C, rpb, c.eps, s)) {
-    set_error("ln_modulate: bad shape");
-    return DDIT_E_INVALID;
-  }
-  if ((rc = launch(P[G_FC1], s))) return rc;
-  if ((rc = launch(P[G_FC2], s))) return rc;
+  if ((rc = attn(r, &a, s))) return rc;
+  if ((rc = launch_g(r, P[G_CPROJ], s))) return rc;
+  if ((rc = ln_mod(r, x, M, mod + 3 * C, mod + 4 * C, rpb, s))) return rc;
+  if ((rc = launch_g(r, P[G_FC1], s))) return rc;
+  if ((rc = launch_g(r, P[G_FC2], s))) return rc;
   return DDIT_OK;
 }
 
@@ -343,10 +399,24 @@ int push_exchange(ddit_req* r, int k, cudaStream_t s) {
     return DDIT_E_CONFIG;
   }
   const int C = r->m->cfg.hidden;
-  if ((k & 1) == 0)
-    exchange_sp_to_tp(r->x_sp, r->peer_tp, g.B, g.T, g.S, C, g.P, g.t_lo, g.Tl, s);
-  else
-    exchange_tp_to_sp(r->x_tp, r->peer_sp, g.B, g.T, g.S, C, g.P, g.s_lo, g.Sl, s);
+  ExchangeSync sync;
+  memset(&sync, 0, sizeof sync);
+  if (r->flags_set) {
+    sync.flags = r->peer_flags;
+    sync.counter = r->counter;
+    sync.rank = g.rank;
+    sync.P = g.P;
+    sync.epoch = ++r->epoch;
+  }
+  int n = 0;
+  timed(r, K_EXCH, s, 0, [&] {
+    if ((k & 1) == 0)
+      n = exchange_sp_to_tp(r->x_sp, r->peer_tp, g.B, g.T, g.S, C, g.P, g.t_lo, g.Tl, sync, s);
+    else
+      n = exchange_tp_to_sp(r->x_tp, r->peer_sp, g.B, g.T, g.S, C, g.P, g.s_lo, g.Sl, sync, s);
+    return 0;
+  });
+  g_launches += (unsigned long long)n;
   return check_cuda("exchange");
 }
 
@@ -451,6 +521,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   r->yemb = reinterpret_cast<bf16*>(ws + r->L.yemb);
   r->kv = reinterpret_cast<bf16*>(ws + r->L.kv);
   r->flags = reinterpret_cast<uint32_t*>(ws + r->L.flags);
+  r->counter = reinterpret_cast<unsigned int*>(ws + r->L.counter);
   r->ts = rflow_timesteps(*d);
   if (d->num_steps > 1000) {
     set_error("num_steps too large");
@@ -465,6 +536,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   }
   cudaMemcpyAsync(r->tv, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(r->flags, 0, kMaxDop * 4, s);
+  cudaMemsetAsync(r->counter, 0, 16, s);
   // tables
   const int base_size = (int)std::lround(std::sqrt((double)g.S));
   const float scale = (float)(std::sqrt((double)d->height * d->width) / c.input_sq_size);
@@ -542,6 +614,7 @@ DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const*
     r->peer_flags.p[q] = flags ? static_cast<uint32_t*>(flags[q]) : nullptr;
   }
   r->peers_set = true;
+  r->flags_set = flags != nullptr;
   return DDIT_OK;
 }
 
@@ -567,6 +640,7 @@ DDIT_API int ddit_step_begin(ddit_req* r, const float* z_local, int step, void* 
   const Geometry& g = r->g;
   const int C = c.hidden, B = g.B;
   // t / fps embedding -> t (temb) -> t_block (tmlp)
+  return timed(r, K_EW, s, 8, [&] {
   timestep_freq(r->freq, r->tv + 4 * step, 2 * B, c.freq_dim, s);
   const float* ft = r->freq;
   const float* ff = r->freq + (size_t)B * c.freq_dim;
@@ -579,6 +653,7 @@ DDIT_API int ddit_step_begin(ddit_req* r, const float* z_local, int step, void* 
   patch_embed(z_local, w.x_emb_w, w.x_emb_b, r->pos, r->x_sp, g.Tl, g.Hl, g.Wl, g.h, g.w, C,
               c.in_channels, B, s);
   return check_cuda("ddit_step_begin");
+  });
 }
 
 DDIT_API int ddit_step_phase(ddit_req* r, int phase, void* stream) {
@@ -595,27 +670,55 @@ DDIT_API int ddit_step_phase(ddit_req* r, int phase, void* stream) {
 
 DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
   if (r->g.P == 1) return DDIT_OK;
-  if (!r->peers_set || !r->peer_flags.p[0]) {
+  if (!r->peers_set || !r->flags_set) {
     set_error("barrier: flags of the group not registered");
     return DDIT_E_CONFIG;
   }
-  r->epoch += 1;
-  flag_barrier(r->peer_flags, r->g.rank, r->g.P, r->epoch, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->g.P, r->epoch, s); });
   return check_cuda("barrier");
 }
+
+DDIT_API int ddit_request_profile(ddit_req* r, int enable) {
+  r->prof_on = enable != 0;
+  r->ev_n = 0;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count) {
+  for (int c = 0; c < K_NCLASS; ++c) {
+    ms[c] = 0.f;
+    count[c] = 0;
+  }
+  if (r->ev_n == 0) return DDIT_OK;
+  if (cudaEventSynchronize(r->ev[2 * r->ev_n - 1]) != cudaSuccess) return check_cuda("profile");
+  for (size_t i = 0; i < r->ev_n; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r->ev[2 * i], r->ev[2 * i + 1]) != cudaSuccess)
+      return check_cuda("profile elapsed");
+    ms[r->ev_cls[i]] += t;
+    count[r->ev_cls[i]] += 1;
+  }
+  r->ev_n = 0;
+  return DDIT_OK;
+}
+
+DDIT_API unsigned long long ddit_launch_count(void) { return g_launches.load(); }
 
 DDIT_API int ddit_step_end(ddit_req* r, float* z_local, int step, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const ddit_model* m = r->m;
   const ddit_config& c = m->cfg;
   const Geometry& g = r->g;
-  if (final_layer(r->x_sp, r->fin, m->w.final_w, m->w.final_b, z_local, g.Tl, g.Hl, g.Wl, g.h, g.w,
-                  c.hidden, c.in_channels, c.out_channels, r->d.guidance, step_dt(r, step), c.eps,
-                  s)) {
-    set_error("final layer: unsupported channel count");
-    return DDIT_E_CONFIG;
-  }
-  return check_cuda("ddit_step_end");
+  return timed(r, K_EW, s, 1, [&] {
+    if (final_layer(r->x_sp, r->fin, m->w.final_w, m->w.final_b, z_local, g.Tl, g.Hl, g.Wl, g.h,
+                    g.w, c.hidden, c.in_channels, c.out_channels, r->d.guidance, step_dt(r, step),
+                    c.eps, s)) {
+      set_error("final layer: unsupported channel count");
+      return (int)DDIT_E_CONFIG;
+    }
+    return check_cuda("ddit_step_end");
+  });
 }
 
 DDIT_API int ddit_dit_step(ddit_req* r, float* z_local, int step, void* stream) {

@@ -1,0 +1,75 @@
+"""One process per GPU: a DoP-P group of ranks running one request's step together.
+
+torch.distributed is only the rendezvous (exchanging 64-byte CUDA IPC handles); the
+sequence-parallel all-to-all itself runs inside libddit as peer stores over NVLink into
+the other ranks' mapped buffers, closed by a flag barrier (csrc/exchange.cu). Reference
+counterpart: the paper's NCCL data plane between engine units; the
+reference simulator models it only as the dit_step(res, dop) curve (profiles.py:69-76).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from ._lib import check, lib
+from .stdit import STDiTModel, StepRequest
+
+
+def ipc_export(ptr: int) -> tuple[bytes, int]:
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    check(lib().ddit_ipc_export(ptr, h, ctypes.byref(off)))
+    return bytes(h.raw), off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    out = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(handle, 64)
+    check(lib().ddit_ipc_import(buf, offset, ctypes.byref(out)))
+    return out.value
+
+
+class GroupStep:
+    """This process's rank of a DoP-``world_size`` group (``group`` or the default group)."""
+
+    def __init__(self, model: STDiTModel, shape, y_cond, group=None, **kw):
+        self.rank = dist.get_rank(group)
+        self.dop = dist.get_world_size(group)
+        self.req = StepRequest(model, shape, y_cond, dop=self.dop, rank=self.rank, **kw)
+        local = self.req.exchange_buffers()
+        mine = [ipc_export(p) for p in local]
+        allh: list = [None] * self.dop
+        dist.all_gather_object(allh, mine, group=group)
+        # every handle is mapped once (the three buffers usually share one allocation)
+        self._imported: list[int] = []
+        cols: list[list[int]] = [[], [], []]
+        for q in range(self.dop):
+            bases: dict[bytes, int] = {}
+            for j in range(3):
+                if q == self.rank:
+                    cols[j].append(local[j])
+                    continue
+                h, off = allh[q][j]
+                if h not in bases:
+                    bases[h] = ipc_import(h, 0)
+                    self._imported.append(bases[h])
+                cols[j].append(bases[h] + off)
+        self.req.set_peers(cols[0], cols[1], cols[2])
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+
+    @property
+    def shard(self):
+        return self.req.shard
+
+    def step(self, z_local: torch.Tensor, step: int, stream=None) -> torch.Tensor:
+        return self.req.step(z_local, step, stream)
+
+    def close(self) -> None:
+        for p in self._imported:
+            lib().ddit_ipc_close(p, 0)
+        self._imported = []
+        self.req.close()

@@ -168,6 +168,25 @@ class StepRequest:
                                                   ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def profile(self, enable: bool) -> None:
+        check(lib().ddit_request_profile(self.handle, 1 if enable else 0))
+
+    def profile_read(self) -> dict[str, tuple[float, int]]:
+        """Per-class (ms, launches) since profiling was enabled: gemm, attention, elementwise,
+        exchange."""
+        ms = (cf * 4)()
+        n = (ci * 4)()
+        check(lib().ddit_request_profile_read(self.handle, ms, n))
+        names = ("gemm", "attention", "elementwise", "exchange")
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
+
+    def step_host(self, z_host: torch.Tensor, step: int, z_dev: torch.Tensor, stream=None) -> torch.Tensor:
+        """End-to-end step through host memory: H2D of z, the step, D2H of z' (in place)."""
+        z_dev.copy_(z_host, non_blocking=True)
+        self.step(z_dev, step, stream)
+        z_host.copy_(z_dev, non_blocking=True)
+        return z_host
+
     def set_peers(self, x_sp: list[int], x_tp: list[int], flags: list[int] | None) -> None:
         n = len(x_sp)
         A = (vp * n)(*x_sp)
@@ -212,3 +231,8 @@ class VirtualGroup:
         for r, z in zip(self.ranks, z_parts):
             r.end(z, step, stream)
         return z_parts
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libddit in this process (bench evidence)."""
+    return int(lib().ddit_launch_count())

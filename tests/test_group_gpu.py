@@ -1,0 +1,22 @@
+"""DoP-2/4 across processes (CUDA IPC peer stores + flag barrier) == single-process DoP 1."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("dop", [2, 4])
+def test_multiprocess_group_matches_dop1(cuda, dop):
+    port = 29600 + dop
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={dop}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "scripts" / "group_check.py"), "144p"]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=ROOT)
+    print(res.stdout[-3000:], res.stderr[-3000:])
+    assert res.returncode == 0
+    assert "PASS" in res.stdout
