@@ -3,12 +3,15 @@
 //   warp 0      : TMA producer (one elected lane) -- A/B k-blocks into a STAGES-deep smem ring
 //   warp 1      : MMA issuer   (one elected lane) -- tcgen05.mma 128xBNx16 into TMEM
 //   warp 2      : TMEM allocator (512 columns: two accumulator buffers at columns 0 / 256)
-//   warps 4..7  : epilogue -- tcgen05.ld (one accumulator row per thread) -> fused op -> global
+//   warps 4..7  : epilogue -- tcgen05.ld (one accumulator row per thread) -> fused op ->
+//                 swizzled smem staging -> TMA store (fp32 residual: TMA load, update, TMA store)
 //
 // The accumulator is double-buffered in TMEM so the epilogue of tile i overlaps the MMAs of
-// tile i+1. Tiles are distributed round-robin over a grid of min(#tiles, #SMs) CTAs.
-// Shapes in the DDiT step: M = tokens (ragged, TMA zero-fills the
-// tail, and the K tail), K in {1152, 4096, 4608}, N in {1152, 2304, 3456, 4608}; N % BN == 0.
+// tile i+1. The epilogue never issues per-row global stores: every output leaves through a
+// TMA bulk tensor store from a 128 B-swizzled (bank-conflict-free) staging buffer, double
+// buffered so the store of sub-tile s overlaps the math of sub-tile s+1.
+// Shapes in the DDiT step: M = tokens (ragged; TMA zero-fills the
+// M and K tails on load and clips on store), K in {288, 1152, 4096, 4608}, N % BN == 0.
 #include "common.cuh"
 #include "gemm_sm100.cuh"
 
@@ -24,17 +27,31 @@ static constexpr int kThreads = 256;
 static constexpr int kTmemCols = 512;
 static constexpr int kAccStride = 256;  // TMEM column offset of accumulator buffer 1
 
-template <int BN>
+template <int BN, int EPI>
+struct EpiCfg {
+  // staging bytes (two buffers) and sub-tile width (columns) per epilogue kind: bf16 outputs
+  // use 64-column sub-tiles (128 B swizzle) when BN allows, else 32 (64 B swizzle)
+  static constexpr bool BF = EPI == EPI_BF16 || EPI == EPI_GELU_BF16;
+  static constexpr int SUB = EPI == EPI_QKV ? 72 : BF ? (BN % 64 == 0 ? 64 : 32) : 32;
+  static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
+  static constexpr int BUF2 = EPI == EPI_RESID ? 128 * 64 : 0;         // bf16 copy (SW64)
+  static constexpr int BYTES = 2 * (BUF + BUF2);
+};
+
+template <int BN, int EPI>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (212 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES;
+  static constexpr int BUDGET = 232448 - 1024 - BAR_BYTES - EpiCfg<BN, EPI>::BYTES;
+  static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EpiCfg<BN, EPI>::BYTES + BAR_BYTES;
   static_assert(B_BYTES % 1024 == 0, "B tile must keep 1024 B swizzle-atom alignment");
   static_assert(BN % 16 == 0 && BN <= 256, "invalid UMMA N");
+  static_assert(BN % EpiCfg<BN, EPI>::SUB == 0, "BN must be a multiple of the epilogue sub-tile");
+  static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
 DDIT_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t* r) {
@@ -43,151 +60,301 @@ DDIT_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t* r) {
                  "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+DDIT_DEV void tmem_ld_x32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
 
-// ------------------------------------------------------------------ epilogues
+DDIT_DEV void tma_store_2d(const void* tmap, const void* smem_src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+DDIT_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+DDIT_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+DDIT_DEV void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+DDIT_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+DDIT_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// 16-byte chunk j of row r in a 128 B-swizzled (Swizzle<3,4,3>) / 64 B-swizzled tile
+DDIT_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
+DDIT_DEV uint32_t sw64(int r, int j) { return (uint32_t)(r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); }
+
+DDIT_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+DDIT_DEV float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+DDIT_DEV float gelu_fast(float x) {
+  // tanh-approximated GELU with the hardware tanh (MUFU.TANH); |err| << bf16 ulp
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.0f + t);
+}
+
+struct EpiCtx {
+  int m_tiles, n_tiles, num_tiles;
+  int M;
+};
+
+// ------------------------------------------------------------------ epilogue: bf16 / gelu / f32
 template <int BN, int EPI>
-DDIT_DEV void epilogue_generic(const EpiParams& ep, uint32_t taddr, int row, int M, int n0) {
-  const bool live = row < M;
+DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
+                             uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
+                             uint64_t* tempty_bar, int lane) {
+  constexpr int SUB = EpiCfg<BN, EPI>::SUB;
+  constexpr int NS = BN / SUB;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    uint32_t r[16];
-    tmem_ld_32x32b_x16(taddr + c, r);
+  for (int sub = 0; sub < NS; ++sub) {
+    uint8_t* sb = sE + (cnt & 1) * EpiCfg<BN, EPI>::BUF;
+    const uint32_t sbase = smem_u32(sb);
+    if (elected) bulk_wait_read<1>();
+    epi_bar();
+    uint32_t r[SUB];
+    tmem_ld_x32(taddr + sub * SUB, r);
+    if constexpr (SUB == 64) tmem_ld_x32(taddr + sub * SUB + 32, r + 32);
     tmem_ld_wait();
-    if (!live) continue;
-    const int col = n0 + c;
-    float v[16];
-    if (ep.bias) {
-      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + col);
+    if (sub == NS - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+    const int col0 = n0 + sub * SUB;
+    float v[SUB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4 b = __ldg(b4 + q);
-        v[4 * q + 0] = __uint_as_float(r[4 * q + 0]) + b.x;
-        v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + b.y;
-        v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + b.z;
-        v[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + b.w;
-      }
+    for (int q = 0; q < SUB / 4; ++q) {
+      float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + q)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * q + 0] = __uint_as_float(r[4 * q + 0]) + b.x;
+      v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + b.y;
+      v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + b.z;
+      v[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + b.w;
+    }
+    if constexpr (EPI == EPI_GELU_BF16) {
+#pragma unroll
+      for (int e = 0; e < SUB; ++e) v[e] = gelu_fast(v[e]);
+    }
+    if constexpr (EPI == EPI_F32) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        st_shared_v4(sbase + sw128(rit, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                     __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+    } else if constexpr (SUB == 32) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(sbase + sw64(rit, j), pack_bf16(v[8 * j], v[8 * j + 1]),
+                     pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                     pack_bf16(v[8 * j + 6], v[8 * j + 7]));
     } else {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+      for (int j = 0; j < 8; ++j)
+        st_shared_v4(sbase + sw128(rit, j), pack_bf16(v[8 * j], v[8 * j + 1]),
+                     pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                     pack_bf16(v[8 * j + 6], v[8 * j + 7]));
     }
-    if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
-      if constexpr (EPI == EPI_GELU_BF16) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = gelu_tanh(v[e]);
-      }
-      uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) +
-                                          (size_t)row * ep.ldo + col);
-      o[0] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                        pack_bf16(v[6], v[7]));
-      o[1] = make_uint4(pack_bf16(v[8], v[9]), pack_bf16(v[10], v[11]), pack_bf16(v[12], v[13]),
-                        pack_bf16(v[14], v[15]));
-    } else if constexpr (EPI == EPI_F32) {
-      float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (size_t)row * ep.ldo + col);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else if constexpr (EPI == EPI_RESID) {
-      float4* rp = reinterpret_cast<float4*>(ep.resid + (size_t)row * ep.ldr + col);
-      float g[16];
-      if (ep.gate) {
-        const float4* g4 =
-            reinterpret_cast<const float4*>(ep.gate + (size_t)(row / ep.rows_per_b) * ep.gate_stride + col);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float4 t = __ldg(g4 + q);
-          g[4 * q] = t.x; g[4 * q + 1] = t.y; g[4 * q + 2] = t.z; g[4 * q + 3] = t.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) g[e] = 1.0f;
-      }
-      float nv[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4 x = rp[q];
-        nv[4 * q + 0] = x.x + g[4 * q + 0] * v[4 * q + 0];
-        nv[4 * q + 1] = x.y + g[4 * q + 1] * v[4 * q + 1];
-        nv[4 * q + 2] = x.z + g[4 * q + 2] * v[4 * q + 2];
-        nv[4 * q + 3] = x.w + g[4 * q + 3] * v[4 * q + 3];
-        rp[q] = make_float4(nv[4 * q], nv[4 * q + 1], nv[4 * q + 2], nv[4 * q + 3]);
-      }
-      if (ep.out2) {
-        uint4* o = reinterpret_cast<uint4*>(ep.out2 + (size_t)row * ep.ldo2 + col);
-        o[0] = make_uint4(pack_bf16(nv[0], nv[1]), pack_bf16(nv[2], nv[3]), pack_bf16(nv[4], nv[5]),
-                          pack_bf16(nv[6], nv[7]));
-        o[1] = make_uint4(pack_bf16(nv[8], nv[9]), pack_bf16(nv[10], nv[11]),
-                          pack_bf16(nv[12], nv[13]), pack_bf16(nv[14], nv[15]));
-      }
+    fence_async_smem();
+    epi_bar();
+    if (elected) {
+      tma_store_2d(tmO, sb, col0, m0);
+      bulk_commit();
     }
+    ++cnt;
   }
 }
 
-// QKV epilogue: the 144-column tile holds two whole heads (head_dim 72) of one of q/k/v.
-// q,k: bias -> per-head RMSNorm (weight) -> optional interleaved RoPE by frame index.
-DDIT_DEV void epilogue_qkv(const EpiParams& ep, uint32_t taddr, int row, int M, int n0) {
-  constexpr int HD = 72;
-  const bool live = row < M;
-  const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
-  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out) + (size_t)row * ep.ldo;
-  int pos = 0;
-  if (ep.rope) pos = (row / ep.rope_S) % ep.rope_T;
+// ------------------------------------------------------------------ epilogue: gated residual
+// x[r, c] += gate[b(r), c] * (acc + bias[c]) in fp32 through TMA (load, update in smem, store),
+// plus an optional bf16 copy of the new x (the cross-attention query input).
+template <int BN>
+struct ResidNext {
+  int m0, n0, sub;
+  bool valid;
+};
+
+template <int BN>
+DDIT_DEV ResidNext<BN> resid_next(int tile, int sub, int n_tiles, int num_tiles) {
+  constexpr int NS = BN / 32;
+  ResidNext<BN> n;
+  if (sub + 1 < NS) {
+    n.sub = sub + 1;
+  } else {
+    n.sub = 0;
+    tile += gridDim.x;
+  }
+  n.valid = tile < num_tiles;
+  n.m0 = (tile / n_tiles) * BM;
+  n.n0 = (tile % n_tiles) * BN;
+  return n;
+}
+
+template <int BN>
+DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const CUtensorMap* tmO2,
+                             uint8_t* sE, uint64_t* rbar, uint32_t taddr, int rit, int tile,
+                             int m0, int n0, const EpiCtx& cx, bool elected, int& cnt,
+                             uint64_t* tempty_bar, int lane) {
+  constexpr int NS = BN / 32;
+  const int row = m0 + rit;
+  const int grow = row < cx.M ? row : cx.M - 1;
+  const float* gate_row = ep.gate ? ep.gate + (size_t)(grow / ep.rows_per_b) * ep.gate_stride : nullptr;
 #pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    const int c0 = h * HD;
-    if (section < 2) {
-      float ss = 0.f;
-#pragma unroll 1
-      for (int j = 0; j < HD / 8; ++j) {
-        uint32_t r[8];
-        tmem_ld_32x32b_x8(taddr + c0 + j * 8, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float v = __uint_as_float(r[e]) + __ldg(ep.bias + n0 + c0 + j * 8 + e);
-          ss += v * v;
-        }
-      }
-      const float inv = rsqrtf(ss * (1.0f / HD) + ep.eps);
-      const float* w = section == 0 ? ep.qnorm_w : ep.knorm_w;
-#pragma unroll 1
-      for (int j = 0; j < HD / 8; ++j) {
-        uint32_t r[8];
-        tmem_ld_32x32b_x8(taddr + c0 + j * 8, r);
-        tmem_ld_wait();
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[e] = (__uint_as_float(r[e]) + __ldg(ep.bias + n0 + c0 + j * 8 + e)) * inv *
-                 __ldg(w + j * 8 + e);
-        if (ep.rope) {
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            float2 cs = __ldg(ep.rope_tab + pos * (HD / 2) + (j * 8 + e) / 2);
-            float a = v[e], b = v[e + 1];
-            v[e] = a * cs.x - b * cs.y;
-            v[e + 1] = b * cs.x + a * cs.y;
-          }
-        }
-        if (live)
-          *reinterpret_cast<uint4*>(out + n0 + c0 + j * 8) =
-              make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                         pack_bf16(v[6], v[7]));
-      }
-    } else {
-#pragma unroll 1
-      for (int j = 0; j < HD / 8; ++j) {
-        uint32_t r[8];
-        tmem_ld_32x32b_x8(taddr + c0 + j * 8, r);
-        tmem_ld_wait();
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[e] = __uint_as_float(r[e]) + __ldg(ep.bias + n0 + c0 + j * 8 + e);
-        if (live)
-          *reinterpret_cast<uint4*>(out + n0 + c0 + j * 8) =
-              make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                         pack_bf16(v[6], v[7]));
+  for (int sub = 0; sub < NS; ++sub) {
+    const int buf = cnt & 1;
+    uint8_t* rb = sE + buf * 16384;
+    uint8_t* ob = sE + 2 * 16384 + buf * 8192;
+    if (elected) {
+      bulk_wait_read<0>();  // buffer buf^1 (previous sub-tile) no longer read by its stores
+      ResidNext<BN> nx = resid_next<BN>(tile, sub, cx.n_tiles, cx.num_tiles);
+      if (nx.valid) {
+        mbar_arrive_expect_tx(&rbar[buf ^ 1], 16384);
+        tma_load_2d(sE + (buf ^ 1) * 16384, tmR, &rbar[buf ^ 1], nx.n0 + nx.sub * 32, nx.m0);
       }
     }
+    mbar_wait(&rbar[buf], (cnt >> 1) & 1);
+    uint32_t r[32];
+    tmem_ld_x32(taddr + sub * 32, r);
+    tmem_ld_wait();
+    if (sub == NS - 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+    const int col0 = n0 + sub * 32;
+    const uint32_t rbase = smem_u32(rb);
+    float nv[32];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 g = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
+                                : make_float4(1.f, 1.f, 1.f, 1.f);
+      const uint32_t a = rbase + sw128(rit, j);
+      const float4 x = ld_shared_f4(a);
+      nv[4 * j + 0] = x.x + g.x * (__uint_as_float(r[4 * j + 0]) + b.x);
+      nv[4 * j + 1] = x.y + g.y * (__uint_as_float(r[4 * j + 1]) + b.y);
+      nv[4 * j + 2] = x.z + g.z * (__uint_as_float(r[4 * j + 2]) + b.z);
+      nv[4 * j + 3] = x.w + g.w * (__uint_as_float(r[4 * j + 3]) + b.w);
+      st_shared_v4(a, __float_as_uint(nv[4 * j]), __float_as_uint(nv[4 * j + 1]),
+                   __float_as_uint(nv[4 * j + 2]), __float_as_uint(nv[4 * j + 3]));
+    }
+    if (ep.out2) {
+      const uint32_t obase = smem_u32(ob);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(obase + sw64(rit, j), pack_bf16(nv[8 * j], nv[8 * j + 1]),
+                     pack_bf16(nv[8 * j + 2], nv[8 * j + 3]), pack_bf16(nv[8 * j + 4], nv[8 * j + 5]),
+                     pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
+    }
+    fence_async_smem();
+    epi_bar();
+    if (elected) {
+      tma_store_2d(tmR, rb, col0, m0);
+      if (ep.out2) tma_store_2d(tmO2, ob, col0, m0);
+      bulk_commit();
+    }
+    ++cnt;
+  }
+}
+
+// ------------------------------------------------------------------ epilogue: QKV
+// The 144-column tile holds two whole heads (head_dim 72) of one of q/k/v.
+// q,k: bias -> per-head RMSNorm (weight) -> optional interleaved RoPE by frame index.
+DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
+                           uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
+                           uint64_t* tempty_bar, int lane) {
+  constexpr int HD = 72;
+  const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
+  const int row = m0 + rit;
+  const int pos = ep.rope ? (row / ep.rope_S) % ep.rope_T : 0;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    uint8_t* sb = sE + (cnt & 1) * EpiCfg<144, EPI_QKV>::BUF;
+    const uint32_t sbase = smem_u32(sb) + rit * 144;
+    if (elected) bulk_wait_read<1>();
+    epi_bar();
+    uint32_t r[72];
+    tmem_ld_x32(taddr + h * HD, r);
+    tmem_ld_x32(taddr + h * HD + 32, r + 32);
+    tmem_ld_32x32b_x8(taddr + h * HD + 64, r + 64);
+    tmem_ld_wait();
+    if (h == 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+    const int c0 = n0 + h * HD;
+    float v[72];
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + c0) + q);
+      v[4 * q + 0] = __uint_as_float(r[4 * q + 0]) + b.x;
+      v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + b.y;
+      v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + b.z;
+      v[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + b.w;
+      ss += v[4 * q] * v[4 * q] + v[4 * q + 1] * v[4 * q + 1] + v[4 * q + 2] * v[4 * q + 2] +
+            v[4 * q + 3] * v[4 * q + 3];
+    }
+    if (section < 2) {
+      const float inv = rsqrtf(ss * (1.0f / HD) + ep.eps);
+      const float* w = section == 0 ? ep.qnorm_w : ep.knorm_w;
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        const float4 wq = __ldg(reinterpret_cast<const float4*>(w) + q);
+        v[4 * q + 0] *= inv * wq.x;
+        v[4 * q + 1] *= inv * wq.y;
+        v[4 * q + 2] *= inv * wq.z;
+        v[4 * q + 3] *= inv * wq.w;
+      }
+      if (ep.rope) {
+        const float4* tab = reinterpret_cast<const float4*>(ep.rope_tab + pos * (HD / 2));
+#pragma unroll
+        for (int q = 0; q < 18; ++q) {  // pairs (4q, 4q+1), (4q+2, 4q+3)
+          const float4 cs = __ldg(tab + q);
+          const float a0 = v[4 * q], a1 = v[4 * q + 1], a2 = v[4 * q + 2], a3 = v[4 * q + 3];
+          v[4 * q + 0] = a0 * cs.x - a1 * cs.y;
+          v[4 * q + 1] = a1 * cs.x + a0 * cs.y;
+          v[4 * q + 2] = a2 * cs.z - a3 * cs.w;
+          v[4 * q + 3] = a3 * cs.z + a2 * cs.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+      st_shared_v4(sbase + j * 16, pack_bf16(v[8 * j], v[8 * j + 1]),
+                   pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                   pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+    fence_async_smem();
+    epi_bar();
+    if (elected) {
+      tma_store_2d(tmO, sb, c0, m0);
+      bulk_commit();
+    }
+    ++cnt;
   }
 }
 
@@ -195,31 +362,42 @@ DDIT_DEV void epilogue_qkv(const EpiParams& ep, uint32_t taddr, int row, int M, 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmO,
+                        const __grid_constant__ CUtensorMap tmR,
+                        const __grid_constant__ CUtensorMap tmO2, int M, int N, int K,
                         const __grid_constant__ EpiParams ep) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + EpiCfg<BN, EPI>::BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int m_tiles = (M + BM - 1) / BM;
-  const int n_tiles = N / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  EpiCtx cx;
+  cx.M = M;
+  cx.m_tiles = (M + BM - 1) / BM;
+  cx.n_tiles = N / BN;
+  cx.num_tiles = cx.m_tiles * cx.n_tiles;
+  const int n_tiles = cx.n_tiles;
+  const int num_tiles = cx.num_tiles;
   const int k_blocks = (K + BK - 1) / BK;  // TMA zero-fills the K tail
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
+    if constexpr (EPI == EPI_RESID) tma_prefetch_desc(&tmR);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -227,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
+      mbar_init(&rbar[i], 1);
     }
     fence_barrier_init();
   }
@@ -292,26 +471,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
+    const int rit = ew * 32 + lane;  // row within the tile
+    const bool elected = (ew == 0 && lane == 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int cnt = 0;
+    if constexpr (EPI == EPI_RESID) {
+      if (elected && (int)blockIdx.x < num_tiles) {  // first residual sub-tile
+        const int t0 = blockIdx.x;
+        mbar_arrive_expect_tx(&rbar[0], 16384);
+        tma_load_2d(sE, &tmR, &rbar[0], (t0 % n_tiles) * BN, (t0 / n_tiles) * BM);
+      }
+    }
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m_blk = tile / n_tiles;
-      const int n_blk = tile % n_tiles;
+      const int m0 = (tile / n_tiles) * BM;
+      const int n0 = (tile % n_tiles) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM + ew * 32 + lane;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
       if constexpr (EPI == EPI_QKV) {
-        epilogue_qkv(ep, taddr, row, M, n_blk * BN);
+        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, &tempty[acc], lane);
+      } else if constexpr (EPI == EPI_RESID) {
+        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, tile, m0, n0, cx, elected, cnt,
+                           &tempty[acc], lane);
       } else {
-        epilogue_generic<BN, EPI>(ep, taddr, row, M, n_blk * BN);
+        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, &tempty[acc], lane);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (elected) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -345,25 +534,26 @@ static PFN_tmapEncodeTiled get_encode() {
   return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld (elements),
-// box = [box_rows, 64 cols], 128 B swizzle, zero fill out of bounds.
-static int make_tmap_bf16(CUtensorMap* m, const void* base, int rows, int cols, int ld,
-                          int box_rows) {
+// 2-D tensor map over a row-major [rows, cols] matrix (row stride ld elements) with box
+// [box_rows, box_cols]; zero fill out of bounds on loads, clipping on stores.
+static int make_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int rows,
+                     int cols, int ld, int box_rows, int box_cols, CUtensorMapSwizzle sw) {
   PFN_tmapEncodeTiled enc = get_encode();
   if (!enc) {
     snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled unavailable");
     return -1;
   }
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * esize};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d) rows=%d cols=%d ld=%d",
-             (int)r, rows, cols, ld);
+    snprintf(g_err, sizeof g_err,
+             "cuTensorMapEncodeTiled failed (%d) rows=%d cols=%d ld=%d box=%dx%d", (int)r, rows,
+             cols, ld, box_rows, box_cols);
     return -1;
   }
   return 0;
@@ -380,18 +570,23 @@ int num_sms() {
   return n;
 }
 
+static bool bn_ok(int bn, int epi) {
+  if (epi == EPI_QKV) return bn == 144;
+  return bn == 96 || bn == 128 || bn == 192 || bn == 256;
+}
+
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
                    int K, int epi, const EpiParams& ep, int bn) {
-  if (bn != 128 && bn != 144 && bn != 192 && bn != 256) {
-    snprintf(g_err, sizeof g_err, "unsupported BN %d", bn);
+  if (!bn_ok(bn, epi)) {
+    snprintf(g_err, sizeof g_err, "unsupported BN %d for epilogue %d", bn, epi);
     return -2;
   }
   if (M <= 0 || N % bn != 0 || K <= 0) {
     snprintf(g_err, sizeof g_err, "bad GEMM shape M=%d N=%d K=%d BN=%d", M, N, K, bn);
     return -2;
   }
-  if (epi == EPI_QKV && (bn != 144 || ep.hidden % 144 != 0)) {
-    snprintf(g_err, sizeof g_err, "EPI_QKV needs BN=144 and hidden %% 144 == 0");
+  if (epi == EPI_QKV && ep.hidden % 144 != 0) {
+    snprintf(g_err, sizeof g_err, "EPI_QKV needs hidden %% 144 == 0");
     return -2;
   }
   if ((lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
@@ -400,8 +595,41 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
     return -2;
   }
   memset(p, 0, sizeof *p);
-  if (make_tmap_bf16(&p->tmA, A, M, K, lda, BM)) return -3;
-  if (make_tmap_bf16(&p->tmB, B, N, K, ldb, bn)) return -3;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  if (make_tmap(&p->tmA, A, BF, 2, M, K, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;
+  if (make_tmap(&p->tmB, B, BF, 2, N, K, ldb, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;
+  switch (epi) {
+    case EPI_BF16:
+    case EPI_GELU_BF16: {
+      const bool wide = bn % 64 == 0;
+      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, N, ep.ldo, BM, wide ? 64 : 32,
+                               wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+        return -3;
+      break;
+    }
+    case EPI_F32:
+      if (!ep.out || make_tmap(&p->tmO, ep.out, F32, 4, M, N, ep.ldo, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return -3;
+      break;
+    case EPI_QKV:
+      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, N, ep.ldo, BM, 72, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return -3;
+      break;
+    case EPI_RESID:
+      if (!ep.resid ||
+          make_tmap(&p->tmR, ep.resid, F32, 4, M, N, ep.ldr, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return -3;
+      if (ep.out2 &&
+          make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+        return -3;
+      p->tmO = p->tmR;
+      if (!ep.out2) p->tmO2 = p->tmR;
+      break;
+    default:
+      snprintf(g_err, sizeof g_err, "unknown epilogue %d", epi);
+      return -2;
+  }
   p->M = M;
   p->N = N;
   p->K = K;
@@ -415,7 +643,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
 
 template <int BN, int EPI>
 static int launch_t(const GemmPlan* p, cudaStream_t s) {
-  constexpr int smem = GemmCfg<BN>::SMEM;
+  constexpr int smem = GemmCfg<BN, EPI>::SMEM;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI>,
@@ -426,8 +654,8 @@ static int launch_t(const GemmPlan* p, cudaStream_t s) {
     }
     attr_set = true;
   }
-  gemm_bf16_tn_kernel<BN, EPI><<<p->grid, kThreads, smem, s>>>(p->tmA, p->tmB, p->M, p->N, p->K,
-                                                                p->ep);
+  gemm_bf16_tn_kernel<BN, EPI><<<p->grid, kThreads, smem, s>>>(p->tmA, p->tmB, p->tmO, p->tmR,
+                                                                p->tmO2, p->M, p->N, p->K, p->ep);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "gemm launch: %s", cudaGetErrorString(e));
@@ -436,27 +664,43 @@ static int launch_t(const GemmPlan* p, cudaStream_t s) {
   return 0;
 }
 
-template <int BN>
-static int launch_bn(const GemmPlan* p, cudaStream_t s) {
-  switch (p->epi) {
-    case EPI_BF16: return launch_t<BN, EPI_BF16>(p, s);
-    case EPI_GELU_BF16: return launch_t<BN, EPI_GELU_BF16>(p, s);
-    case EPI_RESID: return launch_t<BN, EPI_RESID>(p, s);
-    case EPI_F32: return launch_t<BN, EPI_F32>(p, s);
-    default: break;
-  }
-  snprintf(g_err, sizeof g_err, "epilogue %d not instantiated for BN %d", p->epi, BN);
-  return -2;
-}
-
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
-  if (p->epi == EPI_QKV) return launch_t<144, EPI_QKV>(p, s);
-  switch (p->bn) {
-    case 128: return launch_bn<128>(p, s);
-    case 144: return launch_bn<144>(p, s);
-    case 192: return launch_bn<192>(p, s);
-    case 256: return launch_bn<256>(p, s);
+  switch (p->epi) {
+    case EPI_QKV: return launch_t<144, EPI_QKV>(p, s);
+    case EPI_BF16:
+      switch (p->bn) {
+        case 96: return launch_t<96, EPI_BF16>(p, s);
+        case 128: return launch_t<128, EPI_BF16>(p, s);
+        case 192: return launch_t<192, EPI_BF16>(p, s);
+        case 256: return launch_t<256, EPI_BF16>(p, s);
+      }
+      break;
+    case EPI_GELU_BF16:
+      switch (p->bn) {
+        case 96: return launch_t<96, EPI_GELU_BF16>(p, s);
+        case 128: return launch_t<128, EPI_GELU_BF16>(p, s);
+        case 192: return launch_t<192, EPI_GELU_BF16>(p, s);
+        case 256: return launch_t<256, EPI_GELU_BF16>(p, s);
+      }
+      break;
+    case EPI_RESID:
+      switch (p->bn) {
+        case 96: return launch_t<96, EPI_RESID>(p, s);
+        case 128: return launch_t<128, EPI_RESID>(p, s);
+        case 192: return launch_t<192, EPI_RESID>(p, s);
+        case 256: return launch_t<256, EPI_RESID>(p, s);
+      }
+      break;
+    case EPI_F32:
+      switch (p->bn) {
+        case 96: return launch_t<96, EPI_F32>(p, s);
+        case 128: return launch_t<128, EPI_F32>(p, s);
+        case 192: return launch_t<192, EPI_F32>(p, s);
+        case 256: return launch_t<256, EPI_F32>(p, s);
+      }
+      break;
   }
+  snprintf(g_err, sizeof g_err, "epilogue %d not instantiated for BN %d", p->epi, p->bn);
   return -2;
 }
 

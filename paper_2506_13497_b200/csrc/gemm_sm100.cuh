@@ -42,6 +42,9 @@ struct EpiParams {
 struct GemmPlan {
   CUtensorMap tmA;
   CUtensorMap tmB;
+  CUtensorMap tmO;   // epilogue output (bf16 / f32 / qkv)
+  CUtensorMap tmR;   // fp32 residual (EPI_RESID)
+  CUtensorMap tmO2;  // bf16 copy of the residual (EPI_RESID, optional)
   int M, N, K;
   int bn;
   int epi;

@@ -209,14 +209,20 @@ float step_dt(const ddit_req* r, int step) {
   return (float)(dt / 1000.0);
 }
 
+int pick_bn(int n) {
+  for (int bn : {192, 256, 128, 96})
+    if (n % bn == 0) return bn;
+  return 0;
+}
+
 int build_plans(ddit_req* r) {
   const ddit_config& c = r->m->cfg;
   const Geometry& g = r->g;
   const int C = c.hidden;
   const int nblk = 2 * c.depth;
   r->plans.assign((size_t)nblk * G_N, GemmPlan{});
-  const int bn_c = (C % 192 == 0) ? 192 : ((C % 144 == 0) ? 144 : 128);
-  const int bn_mlp = (c.mlp_hidden % 256 == 0) ? 256 : ((c.mlp_hidden % 192 == 0) ? 192 : 144);
+  const int bn_c = pick_bn(C);
+  const int bn_mlp = c.mlp_hidden % 256 == 0 ? 256 : pick_bn(c.mlp_hidden);
   for (int k = 0; k < nblk; ++k) {
     const bool temporal = k & 1;
     const int M = temporal ? g.M_tp : g.M_sp;
@@ -555,7 +561,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   e.out = yhid;
   e.ldo = c.hidden;
   if ((rc = gemm_plan_init(&gp, ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly,
-                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, 144)) ||
+                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, pick_bn(c.hidden))) ||
       (rc = launch(gp, s))) {
     set_error("y_embedder fc1: %s", gemm_last_error());
     delete r;
@@ -564,7 +570,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   e.bias = m->w.y2_b;
   e.out = r->yemb;
   if ((rc = gemm_plan_init(&gp, yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden,
-                           EPI_BF16, e, 144)) ||
+                           EPI_BF16, e, pick_bn(c.hidden))) ||
       (rc = launch(gp, s))) {
     set_error("y_embedder fc2: %s", gemm_last_error());
     delete r;
@@ -577,7 +583,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
     e.out = r->kv + (size_t)k * Ly * 2 * c.hidden;
     e.ldo = 2 * c.hidden;
     if ((rc = gemm_plan_init(&gp, r->yemb, c.hidden, m->blocks[k].ckv_w, c.hidden, Ly,
-                             2 * c.hidden, c.hidden, EPI_BF16, e, 144)) ||
+                             2 * c.hidden, c.hidden, EPI_BF16, e, pick_bn(2 * c.hidden))) ||
         (rc = launch(gp, s))) {
       set_error("cross kv: %s", gemm_last_error());
       delete r;

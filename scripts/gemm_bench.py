@@ -10,7 +10,7 @@ from paper_2506_13497_b200 import _lib, kernels
 
 dev = torch.device("cuda:0")
 M = 2 * 6075
-shapes = [("qkv", 3456, 1152, 144, _lib.EPI_BF16), ("proj", 1152, 1152, 128, _lib.EPI_BF16),
+shapes = [("qkv", 3456, 1152, 192, _lib.EPI_BF16), ("proj", 1152, 1152, 128, _lib.EPI_BF16),
           ("fc1", 4608, 1152, 256, _lib.EPI_GELU_BF16), ("fc2", 1152, 4608, 128, _lib.EPI_BF16),
           ("fc1_192", 4608, 1152, 192, _lib.EPI_GELU_BF16), ("proj192", 1152, 1152, 192, _lib.EPI_BF16),
           ("big", 8192, 8192, 256, _lib.EPI_BF16)]

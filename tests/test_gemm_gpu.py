@@ -21,8 +21,9 @@ def _inputs(M, N, K, dev, seed=0):
     return a, w, bias
 
 
-@pytest.mark.parametrize("bn", [128, 144, 192, 256])
-@pytest.mark.parametrize("M,N,K", [(128, 1152, 64), (300, 2304, 1152), (1000, 4608, 1152), (777, 1152, 4608)])
+@pytest.mark.parametrize("bn", [96, 128, 192, 256])
+@pytest.mark.parametrize("M,N,K", [(128, 1152, 64), (300, 2304, 1152), (1000, 4608, 1152),
+                                   (777, 1152, 4608), (200, 288, 288), (5, 576, 104)])
 def test_gemm_bias_bf16(cuda, bn, M, N, K):
     from paper_2506_13497_b200 import kernels, _lib
 
@@ -46,20 +47,25 @@ def test_gemm_f32_and_gelu(cuda):
     assert rel_l2(out, torch.nn.functional.gelu(ref, approximate="tanh")) < 5e-3
 
 
-def test_gemm_resid_gate(cuda):
+@pytest.mark.parametrize("bn,N,K", [(128, 1152, 1152), (192, 1152, 4608), (96, 288, 1152), (256, 2304, 288)])
+def test_gemm_resid_gate(cuda, bn, N, K):
     from paper_2506_13497_b200 import kernels, _lib
 
-    M, N, K = 2 * 607, 1152, 1152
+    M = 2 * 607
     a, w, bias = _inputs(M, N, K, cuda, seed=2)
     x = torch.randn(M, N, device=cuda)
     gate = torch.randn(2, N, device=cuda)
     x0 = x.clone()
     out2 = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
-    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, out2=out2, bn=128)
+    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, out2=out2, bn=bn)
     b = torch.arange(M, device=cuda) // (M // 2)
     ref = x0 + gate[b] * (a.float() @ w.float().T + bias)
     assert rel_l2(x, ref) < 1e-5
     assert rel_l2(out2, ref) < 5e-3
+    # no gate, no bf16 copy
+    x1 = x0.clone()
+    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x1, bn=bn)
+    assert rel_l2(x1, x0 + a.float() @ w.float().T + bias) < 1e-5
 
 
 @pytest.mark.parametrize("rope", [False, True])
