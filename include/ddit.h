@@ -165,7 +165,8 @@ DDIT_API void ddit_model_destroy(ddit_model* m);
 /* Bytes of device workspace a request needs (caller allocates, 256-byte aligned). */
 DDIT_API int ddit_request_workspace_bytes(const ddit_model* m, const ddit_req_desc* d,
                                           uint64_t* bytes);
-/* Shard of this rank: frames [t_lo, t_hi) (spatial phase) and tokens [s_lo, s_hi) (temporal). */
+/* Shard of this rank: frames [t_lo, t_hi) (spatial phase) and tokens [s_lo, s_hi) (temporal).
+ * Pure host arithmetic (m may be NULL): rank r owns [r*ceil(X/P), (r+1)*ceil(X/P)) ∩ [0, X). */
 DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int* t_lo, int* t_hi,
                                 int* s_lo, int* s_hi);
 /* Opens a request: builds tables, embeds the caption y_cond (device fp32 [300, 4096]) together

@@ -477,7 +477,9 @@ DDIT_API int ddit_request_workspace_bytes(const ddit_model* m, const ddit_req_de
 DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int* t_lo, int* t_hi,
                                 int* s_lo, int* s_hi) {
   Geometry g;
-  int rc = geometry(m->cfg, *d, &g);
+  ddit_config none;
+  memset(&none, 0, sizeof none);
+  int rc = geometry(m ? m->cfg : none, *d, &g);  // pure host math: model may be NULL
   if (rc) return rc;
   *t_lo = g.t_lo;
   *t_hi = g.t_hi;

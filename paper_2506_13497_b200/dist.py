@@ -32,6 +32,30 @@ def ipc_import(handle: bytes, offset: int) -> int:
     return out.value
 
 
+def assemble_peer_table(rank: int, dop: int, local: tuple[int, int, int], gathered: list,
+                        importer=None) -> tuple[list[list[int]], list[int]]:
+    """Per-rank pointer table of the three exchange buffers (x_sp, x_tp, flags).
+
+    ``gathered[q]`` = rank q's [(ipc_handle, offset)] * 3. Own buffers are used directly;
+    every distinct peer allocation is mapped once (``importer(handle) -> base``) and the
+    three pointers are base + offset. Returns (columns, imported bases)."""
+    importer = importer or (lambda h: ipc_import(h, 0))
+    imported: list[int] = []
+    cols: list[list[int]] = [[], [], []]
+    for q in range(dop):
+        bases: dict[bytes, int] = {}
+        for j in range(3):
+            if q == rank:
+                cols[j].append(local[j])
+                continue
+            h, off = gathered[q][j]
+            if h not in bases:
+                bases[h] = importer(h)
+                imported.append(bases[h])
+            cols[j].append(bases[h] + off)
+    return cols, imported
+
+
 class GroupStep:
     """This process's rank of a DoP-``world_size`` group (``group`` or the default group)."""
 
@@ -43,20 +67,7 @@ class GroupStep:
         mine = [ipc_export(p) for p in local]
         allh: list = [None] * self.dop
         dist.all_gather_object(allh, mine, group=group)
-        # every handle is mapped once (the three buffers usually share one allocation)
-        self._imported: list[int] = []
-        cols: list[list[int]] = [[], [], []]
-        for q in range(self.dop):
-            bases: dict[bytes, int] = {}
-            for j in range(3):
-                if q == self.rank:
-                    cols[j].append(local[j])
-                    continue
-                h, off = allh[q][j]
-                if h not in bases:
-                    bases[h] = ipc_import(h, 0)
-                    self._imported.append(bases[h])
-                cols[j].append(bases[h] + off)
+        cols, self._imported = assemble_peer_table(self.rank, self.dop, local, allh)
         self.req.set_peers(cols[0], cols[1], cols[2])
         torch.cuda.synchronize()
         dist.barrier(group=group)

@@ -88,3 +88,22 @@ def test_virtual_dop_matches_dop1(cuda, dop):
     zp = torch.cat(parts, dim=2)
     torch.cuda.synchronize()
     assert torch.equal(zp, z1), f"max diff {(zp - z1).abs().max().item()}"
+
+
+@pytest.mark.parametrize("step", [0, 17, 29])
+def test_tiny_step_matches_golden_fixture(cuda, step):
+    """Against the committed oracle vectors (tests/golden/stdit_tiny_golden.pt) -- no oracle
+    run needed on the GPU box."""
+    from pathlib import Path
+
+    from paper_2506_13497_b200 import shapes, weights
+
+    g = torch.load(Path(__file__).parent / "golden" / "stdit_tiny_golden.pt")
+    cfg = weights.TINY
+    W = weights.init_weights(cfg, seed=3)
+    sh = shapes.shape_of("144p-16f")
+    z, y = weights.synthetic_inputs(cfg, sh.latent)
+    assert torch.equal(z, g["z"])
+    out = _gpu(cfg, W, sh, z, y, step, cuda)
+    ref = g[f"z_{step}"]
+    assert rel_l2(out, ref) <= 1e-2 and rel_l2(out - z, ref - z) <= 2e-2
