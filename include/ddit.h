@@ -94,6 +94,9 @@ typedef struct ddit_attn {
 } ddit_attn;
 
 DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
+/* Short-sequence (T <= 32) temporal attention: q/k/v must be the three sections of one
+ * row-major QKV matrix and share one index map; one CTA per (batch, token position). */
+DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
 
 /* ------------------------------------------------------------------ the STDiT3 step
  * Model = device weights (caller-owned, registered by pointer). Request = one video being

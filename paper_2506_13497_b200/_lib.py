@@ -118,6 +118,7 @@ class Attn(ctypes.Structure):
 
 _SIGNATURES = {
     "ddit_attention": [ctypes.POINTER(Attn), vp],
+    "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
     "ddit_model_create": [ctypes.POINTER(CConfig), ctypes.POINTER(CWeights), ctypes.POINTER(vp)],
     "ddit_request_workspace_bytes": [vp, ctypes.POINTER(CReqDesc), ctypes.POINTER(ctypes.c_uint64)],
     "ddit_request_shard": [vp, ctypes.POINTER(CReqDesc)] + [ctypes.POINTER(ci)] * 4,

@@ -26,6 +26,7 @@
 
 namespace ddit {
 int attention_launch(const ddit_attn* a, cudaStream_t s);
+int temporal_attention_launch(const ddit_attn* a, cudaStream_t s);
 }
 
 using namespace ddit;
@@ -326,6 +327,10 @@ int ln_mod(ddit_req* r, float* x, int M, const float* shift, const float* scale,
 int attn(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
   return timed(r, K_ATTN, s, 1, [&] { return attention_launch(a, s); });
 }
+int attn_temporal(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
+  if (a->Lq > 32) return attn(r, a, s);
+  return timed(r, K_ATTN, s, 1, [&] { return temporal_attention_launch(a, s); });
+}
 
 int run_block(ddit_req* r, int k, cudaStream_t s) {
   const ddit_config& c = r->m->cfg;
@@ -366,7 +371,7 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
     a.q_inner_stride = a.kv_inner_stride = 1;
     a.q_tok = a.kv_tok = g.Sl;
   }
-  if ((rc = attn(r, &a, s))) return rc;
+  if ((rc = temporal ? attn_temporal(r, &a, s) : attn(r, &a, s))) return rc;
   if ((rc = launch_g(r, P[G_PROJ], s))) return rc;
   if ((rc = launch_g(r, P[G_CQ], s))) return rc;
   // cross attention: each batch's rows attend to its own 300 text tokens

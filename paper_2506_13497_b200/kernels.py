@@ -77,7 +77,8 @@ def gemm(
 
 
 def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
-              q_map=(1, 0, 0, 1), kv_map=(1, 0, 0, 1), scale: float | None = None, stream=None):
+              q_map=(1, 0, 0, 1), kv_map=(1, 0, 0, 1), scale: float | None = None, stream=None,
+              temporal: bool = False):
     """Flash attention over token-major bf16 matrices; maps = (inner, outer, inner_stride, tok)."""
     a = Attn()
     a.q, a.ldq = ptr(q), q.stride(0)
@@ -88,5 +89,6 @@ def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
     a.q_inner, a.q_outer, a.q_inner_stride, a.q_tok = q_map
     a.kv_inner, a.kv_outer, a.kv_inner_stride, a.kv_tok = kv_map
     a.scale = scale if scale is not None else 72 ** -0.5
-    check(lib().ddit_attention(ctypes.byref(a), stream_ptr(stream)))
+    fn = lib().ddit_attention_temporal if temporal else lib().ddit_attention
+    check(fn(ctypes.byref(a), stream_ptr(stream)))
     return o

@@ -30,8 +30,11 @@ def test_spatial(cuda, B, T, S):
     assert rel_l2(o, ref) < 1e-2
 
 
-@pytest.mark.parametrize("B,T,Sl", [(2, 15, 405), (2, 30, 17), (1, 4, 3), (2, 70, 5)])
-def test_temporal(cuda, B, T, Sl):
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("B,T,Sl", [(2, 15, 405), (2, 30, 17), (1, 4, 3), (2, 70, 5), (2, 16, 9), (1, 32, 2), (2, 1, 3)])
+def test_temporal(cuda, B, T, Sl, fast):
+    if fast and T > 32:
+        pytest.skip("short-sequence kernel is for T <= 32")
     from paper_2506_13497_b200 import kernels
     g = torch.Generator().manual_seed(1)
     M = B * T * Sl
@@ -40,7 +43,7 @@ def test_temporal(cuda, B, T, Sl):
     o = torch.zeros(M, C, device=cuda, dtype=torch.bfloat16)
     mp = (Sl, T * Sl, 1, Sl)
     kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=H, num_seqs=B * Sl,
-                      Lq=T, Lk=T, q_map=mp, kv_map=mp)
+                      Lq=T, Lk=T, q_map=mp, kv_map=mp, temporal=fast)
     x = qkv.view(B, T, Sl, 3, H, D).transpose(1, 2).reshape(B * Sl, T, 3, H, D)
     q, k, v = x.unbind(2)
     ref = ref_attn(q, k, v).reshape(B, Sl, T, C).transpose(1, 2).reshape(M, C)
