@@ -97,6 +97,10 @@ DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
 /* Short-sequence (T <= 32) temporal attention: q/k/v must be the three sections of one
  * row-major QKV matrix and share one index map; one CTA per (batch, token position). */
 DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
+/* tcgen05 / TMEM flash attention (spatial and cross attention): contiguous sequences
+ * (tok == 1, inner <= 1), row strides and head offsets in whole 72-column slots, k and v in one
+ * matrix. Returns DDIT_E_INVALID for layouts it does not cover. */
+DDIT_API int ddit_attention_tc(const ddit_attn* a, void* stream);
 
 /* ------------------------------------------------------------------ the STDiT3 step
  * Model = device weights (caller-owned, registered by pointer). Request = one video being
@@ -199,6 +203,11 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream);
 
 /* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
+
+/* Request options: DDIT_OPT_TC_ATTENTION (default 1) selects the tcgen05 FMHA for spatial /
+ * cross attention; 0 falls back to the mma.sync flash kernel (kept as the baseline). */
+#define DDIT_OPT_TC_ATTENTION 1
+DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value);
 
 /* Profiling: while enabled every launch of the request is bracketed by CUDA events on its
  * stream; _read returns per-class totals (ms, launches) for classes

@@ -119,6 +119,7 @@ class Attn(ctypes.Structure):
 _SIGNATURES = {
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
+    "ddit_attention_tc": [ctypes.POINTER(Attn), vp],
     "ddit_model_create": [ctypes.POINTER(CConfig), ctypes.POINTER(CWeights), ctypes.POINTER(vp)],
     "ddit_request_workspace_bytes": [vp, ctypes.POINTER(CReqDesc), ctypes.POINTER(ctypes.c_uint64)],
     "ddit_request_shard": [vp, ctypes.POINTER(CReqDesc)] + [ctypes.POINTER(ci)] * 4,
@@ -133,6 +134,7 @@ _SIGNATURES = {
     "ddit_step_barrier": [vp, vp],
     "ddit_request_timestep": [vp, ci, ctypes.POINTER(cf), ctypes.POINTER(cf)],
     "ddit_request_profile": [vp, ci],
+    "ddit_request_set_option": [vp, ci, ci],
     "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
     "ddit_ipc_export": [vp, vp, ctypes.POINTER(ctypes.c_uint64)],
     "ddit_ipc_import": [vp, ctypes.c_uint64, ctypes.POINTER(vp)],

@@ -1,0 +1,451 @@
+// tcgen05 / TMEM flash attention (forward, non-causal, head_dim 72) for the STDiT3 spatial
+// and cross attention.
+//
+// One CTA = one (sequence, head, 128-query tile). Warp roles:
+//   warp 0     : TMA producer. Q/K/V come straight out of the token-major QKV (or q / kv)
+//                matrices through 4-D tensor maps {72, head slot, token, sequence}: the token
+//                dimension is clipped at the sequence length, so ragged tiles zero-fill on load
+//                and clip on store. head_dim 72 is split into a 64-column 128B-swizzled box and
+//                a 16-column 32B-swizzled box whose columns 72..79 fall outside the map (zeros).
+//   warp 1     : MMA issuer (one thread). S_j = Q K_j^T (M128 N128, K = 4 x16 SW128 + 1 x16 SW32)
+//                into a double-buffered TMEM S; O += P_j V_j with V as an MN-major B operand
+//                (N64 SW128 + N16 SW32, 8 k-steps of 16 keys) into TMEM O. QK_{j+1} is issued
+//                before PV_j so the tensor core computes the next scores while softmax runs.
+//   warps 4-7  : softmax, one query row per thread (= TMEM lane): online softmax in fp32 with
+//                exp2, lazy O rescaling (only when the running max grows by > 2^8), P written as
+//                bf16 into 128B-swizzled smem (the A operand of PV); final O / l -> bf16 -> smem
+//                -> TMA store.
+// TMEM: S0 [0,128), S1 [128,256), O [256,336) of a 512-column allocation.
+#include "common.cuh"
+#include "ddit.h"
+#include "capi_internal.h"
+#include "fmha_plan.cuh"
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+namespace ddit {
+
+namespace fm {
+constexpr int BQ = 128, BKV = 128, THREADS = 256, STAGES = 2;
+constexpr int QA = 16384, QB = 4096;                 // Q: 64-col SW128 + 16-col SW32 boxes
+constexpr int KA = 16384, KB = 4096, VA = 16384, VB = 4096;
+constexpr int STAGE = KA + KB + VA + VB;             // 40 KB
+constexpr int PBUF = 2 * 16384;                      // P: two 64-key SW128 regions
+constexpr int OFF_Q = 0;
+constexpr int OFF_KV = QA + QB;                      // 20480 (1024-aligned)
+constexpr int OFF_P = OFF_KV + STAGES * STAGE;       // 102400
+constexpr int OFF_BAR = OFF_P + 2 * PBUF;            // 167936
+constexpr int SMEM = 1024 + OFF_BAR + 256;
+constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O = 256;
+constexpr float RESCALE_LOG2 = 8.0f;
+}  // namespace fm
+
+
+DDIT_DEV void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+DDIT_DEV void tma_store_4d(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
+// smem matrix descriptor: start, LBO (bytes), SBO (bytes), layout (2 = SW128, 6 = SW32)
+DDIT_DEV uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+DDIT_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DDIT_DEV void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+DDIT_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+DDIT_DEV void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+DDIT_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+DDIT_DEV void st_shared_u4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+DDIT_DEV float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(fm::THREADS, 1)
+    fmha_sm100_kernel(const __grid_constant__ CUtensorMap tmQa,
+                      const __grid_constant__ CUtensorMap tmQb,
+                      const __grid_constant__ CUtensorMap tmKVa,
+                      const __grid_constant__ CUtensorMap tmKVb,
+                      const __grid_constant__ CUtensorMap tmO,
+                      const __grid_constant__ FmhaParams p) {
+  using namespace fm;
+  extern __shared__ uint8_t fm_smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fm_smem_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [STAGES]
+  uint64_t* kv_empty = bars + 3;  // [STAGES]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_free = bars + 7;    // [2]
+  uint64_t* p_full = bars + 9;    // [2]
+  uint64_t* pv_done = bars + 11;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int q0 = blockIdx.x * BQ, head = blockIdx.y, seq = blockIdx.z;
+  const int nk = (p.Lk + BKV - 1) / BKV;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQa);
+    tma_prefetch_desc(&tmQb);
+    tma_prefetch_desc(&tmKVa);
+    tma_prefetch_desc(&tmKVb);
+    tma_prefetch_desc(&tmO);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(q_full, QA + QB);
+      tma_load_4d(sm + OFF_Q, &tmQa, q_full, 0, p.q_slot + head, q0, seq);
+      tma_load_4d(sm + OFF_Q + QA, &tmQb, q_full, 64, p.q_slot + head, q0, seq);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
+        uint8_t* base = sm + OFF_KV + st * STAGE;
+        mbar_arrive_expect_tx(&kv_full[st], STAGE);
+        tma_load_4d(base, &tmKVa, &kv_full[st], 0, p.k_slot + head, j * BKV, seq);
+        tma_load_4d(base + KA, &tmKVb, &kv_full[st], 64, p.k_slot + head, j * BKV, seq);
+        tma_load_4d(base + KA + KB, &tmKVa, &kv_full[st], 0, p.v_slot + head, j * BKV, seq);
+        tma_load_4d(base + KA + KB + VA, &tmKVb, &kv_full[st], 64, p.v_slot + head, j * BKV, seq);
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+    constexpr uint32_t id_qk = idesc_f16(128, 128, false);
+    constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
+    constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
+    const uint32_t qa = smem_u32(sm + OFF_Q), qb = qa + QA;
+    auto issue_qk = [&](int j) {
+      const int st = j % STAGES;
+      const uint32_t ka = smem_u32(sm + OFF_KV + st * STAGE), kb = ka + KA;
+      const uint32_t d = tmem + ((j & 1) ? TM_S1 : TM_S0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        umma_bf16_ss(d, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2), id_qk, k > 0);
+      umma_bf16_ss(d, sdesc(qb, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
+      umma_commit(&s_full[j & 1]);
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) issue_qk(0);
+    __syncwarp();
+    for (int j = 0; j < nk; ++j) {
+      if (j + 1 < nk) {
+        const int jn = j + 1;
+        mbar_wait(&kv_full[jn % STAGES], (jn / STAGES) & 1);
+        if (jn >= 2) mbar_wait(&s_free[jn & 1], ((jn - 2) >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) issue_qk(jn);
+        __syncwarp();
+      }
+      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const int st = j % STAGES;
+        const uint32_t va = smem_u32(sm + OFF_KV + st * STAGE + KA + KB), vb = va + VA;
+        const uint32_t pb = smem_u32(sm + OFF_P + (j & 1) * PBUF);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+          const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+          umma_bf16_ss(tmem + TM_O, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
+          umma_bf16_ss(tmem + TM_O + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+        }
+        umma_commit(&pv_done[j & 1]);
+        umma_commit(&kv_empty[j % STAGES]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ softmax
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
+    float m = -INFINITY, l = 0.f;
+    int pv_known = -1;  // highest PV index known complete
+    for (int j = 0; j < nk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t s[128];
+      const uint32_t sadr = lane_base + ((j & 1) ? TM_S1 : TM_S0);
+      tmem_ld32(sadr, s);
+      tmem_ld32(sadr + 32, s + 32);
+      tmem_ld32(sadr + 64, s + 64);
+      tmem_ld32(sadr + 96, s + 96);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[j & 1]);
+      const int valid = min(BKV, p.Lk - j * BKV);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 128; ++e)
+        if (e < valid) mx = fmaxf(mx, __uint_as_float(s[e]));
+      const float m_new = fmaxf(m, mx * p.scale_log2);
+      const bool resc = m_new > m + RESCALE_LOG2;
+      float alpha = 1.f;
+      if (resc) {
+        alpha = fast_exp2(m - m_new);
+        m = m_new;
+        l *= alpha;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        pv_known = j - 1;
+        tc_fence_after();
+        uint32_t o[80];
+        tmem_ld32(lane_base + TM_O, o);
+        tmem_ld32(lane_base + TM_O + 32, o + 32);
+        tmem_ld16(lane_base + TM_O + 64, o + 64);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 80; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+        tmem_st32(lane_base + TM_O, o);
+        tmem_st32(lane_base + TM_O + 32, o + 32);
+        tmem_st16(lane_base + TM_O + 64, o + 64);
+        tmem_st_wait();
+      }
+      if (j >= 2 && pv_known < j - 2) {  // P buffer (j & 1) was read by PV_{j-2}
+        mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
+        pv_known = j - 2;
+      }
+      const uint32_t pbase = smem_u32(sm + OFF_P + (j & 1) * PBUF);
+      const float neg_m = -m;
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys
+        float pv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int key = c * 8 + e;
+          pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
+          rs += pv[e];
+        }
+        const uint32_t addr = pbase + (c >> 3) * 16384 + (uint32_t)(row * 128 + (((c & 7) ^ (row & 7)) << 4));
+        st_shared_u4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
+                     pack_bf16(pv[6], pv[7]));
+      }
+      l += rs;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    // ---- epilogue: O / l -> bf16 -> smem (144 B rows) -> TMA store (clipped at Lq)
+    mbar_wait(&pv_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+    tc_fence_after();
+    uint32_t o[80];
+    tmem_ld32(lane_base + TM_O, o);
+    tmem_ld32(lane_base + TM_O + 32, o + 32);
+    tmem_ld16(lane_base + TM_O + 64, o + 64);
+    tmem_ld_wait();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const uint32_t obase = smem_u32(sm + OFF_P) + row * 144;
+#pragma unroll
+    for (int c = 0; c < 9; ++c)
+      st_shared_u4(obase + c * 16,
+                   pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+                   pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+                   pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+                   pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (ew == 0 && lane == 0) {
+      tma_store_4d(&tmO, sm + OFF_P, 0, p.o_slot + head, q0, seq);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encode encoder() {
+  static PFN_encode fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encode>(ptr);
+  });
+  return fn;
+}
+
+// View of a token-major bf16 matrix as {72 (d), slots, L tokens, seqs}.
+static bool map4d(CUtensorMap* m, const void* base, int slots, int L, int seqs, size_t row_bytes,
+                  size_t seq_bytes, int box0, CUtensorMapSwizzle sw) {
+  PFN_encode enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {72, (cuuint64_t)slots, (cuuint64_t)L, (cuuint64_t)seqs};
+  cuuint64_t strides[3] = {144, (cuuint64_t)row_bytes, (cuuint64_t)seq_bytes};
+  cuuint32_t box[4] = {(cuuint32_t)box0, 1, 128, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Whether the tcgen05 path applies: contiguous sequences (tok == 1, inner == 1), strides and
+// head offsets in whole 72-column slots, k and v in one matrix.
+bool fmha_supported(const ddit_attn* a) {
+  if (a->head_dim != 72) return false;
+  if (a->q_tok != 1 || a->kv_tok != 1) return false;
+  if ((a->q_inner > 1) || (a->kv_inner > 1)) return false;
+  if (a->ldq % 72 || a->ldk % 72 || a->ldo % 72 || a->ldv != a->ldk) return false;
+  const auto* k = static_cast<const __nv_bfloat16*>(a->k);
+  const auto* v = static_cast<const __nv_bfloat16*>(a->v);
+  if (v < k || (v - k) % 72) return false;
+  auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  return al(a->q) && al(a->k) && al(a->o);
+}
+
+int fmha_plan_init(FmhaPlan* fp, const ddit_attn* a) {
+  if (!fmha_supported(a)) {
+    set_error("fmha: layout not supported by the tcgen05 path");
+    return DDIT_E_INVALID;
+  }
+  memset(fp, 0, sizeof *fp);
+  // slot extents cover exactly the heads used (k, v share one map: v = k + v_slot slots)
+  const int v_slot = (int)((static_cast<const __nv_bfloat16*>(a->v) -
+                            static_cast<const __nv_bfloat16*>(a->k)) / 72);
+  const int q_slots = a->heads, kv_slots = v_slot + a->heads, o_slots = a->heads;
+  const size_t q_seq = (size_t)a->q_outer * a->ldq * 2, kv_seq = (size_t)a->kv_outer * a->ldk * 2;
+  const size_t o_seq = (size_t)a->q_outer * a->ldo * 2;
+  bool ok = map4d(&fp->tmQa, a->q, q_slots, a->Lq, a->num_seqs, (size_t)a->ldq * 2, q_seq, 64,
+                  CU_TENSOR_MAP_SWIZZLE_128B) &&
+            map4d(&fp->tmQb, a->q, q_slots, a->Lq, a->num_seqs, (size_t)a->ldq * 2, q_seq, 16,
+                  CU_TENSOR_MAP_SWIZZLE_32B) &&
+            map4d(&fp->tmKVa, a->k, kv_slots, a->Lk, a->num_seqs, (size_t)a->ldk * 2, kv_seq, 64,
+                  CU_TENSOR_MAP_SWIZZLE_128B) &&
+            map4d(&fp->tmKVb, a->k, kv_slots, a->Lk, a->num_seqs, (size_t)a->ldk * 2, kv_seq, 16,
+                  CU_TENSOR_MAP_SWIZZLE_32B) &&
+            map4d(&fp->tmO, a->o, o_slots, a->Lq, a->num_seqs, (size_t)a->ldo * 2, o_seq, 72,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!ok) {
+    set_error("fmha: cuTensorMapEncodeTiled failed");
+    return DDIT_E_TMA;
+  }
+  fp->p.Lq = a->Lq;
+  fp->p.Lk = a->Lk;
+  fp->p.q_slot = 0;
+  fp->p.k_slot = 0;
+  fp->p.v_slot = v_slot;
+  fp->p.o_slot = 0;
+  fp->p.scale_log2 = a->scale * 1.4426950408889634f;
+  fp->grid = dim3((a->Lq + fm::BQ - 1) / fm::BQ, a->heads, a->num_seqs);
+  return DDIT_OK;
+}
+
+int fmha_plan_launch(const FmhaPlan* fp, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fmha_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    attr = true;
+  }
+  fmha_sm100_kernel<<<fp->grid, fm::THREADS, fm::SMEM, s>>>(fp->tmQa, fp->tmQb, fp->tmKVa,
+                                                             fp->tmKVb, fp->tmO, fp->p);
+  return check_cuda("fmha_sm100_kernel");
+}
+
+}  // namespace ddit
+
+extern "C" DDIT_API int ddit_attention_tc(const ddit_attn* a, void* stream) {
+  ddit::FmhaPlan fp;
+  int rc = ddit::fmha_plan_init(&fp, a);
+  if (rc) return rc;
+  return ddit::fmha_plan_launch(&fp, static_cast<cudaStream_t>(stream));
+}

@@ -24,6 +24,7 @@
 #include "exchange.cuh"
 #include "gemm_sm100.cuh"
 
+#include "fmha_plan.cuh"
 namespace ddit {
 int attention_launch(const ddit_attn* a, cudaStream_t s);
 int temporal_attention_launch(const ddit_attn* a, cudaStream_t s);
@@ -143,10 +144,14 @@ struct ddit_req {
   unsigned int* counter;
   std::vector<float> ts;  // transformed timesteps
   std::vector<GemmPlan> plans;  // [2*depth][G_N]
+  std::vector<FmhaPlan> fm_self;   // [2*depth] tcgen05 self-attention plans (spatial blocks)
+  std::vector<FmhaPlan> fm_cross;  // [2*depth] tcgen05 cross-attention plans
+  std::vector<uint8_t> fm_self_ok, fm_cross_ok;
   PeerPtrs peer_sp{}, peer_tp{};
   PeerFlags peer_flags{};
   bool peers_set = false;
   bool flags_set = false;
+  bool use_tc_attention = true;  // tcgen05 FMHA for spatial / cross attention
   uint32_t epoch = 0;
   // profiling: event pairs around every launch, tagged by kernel class
   bool prof_on = false;
@@ -332,20 +337,11 @@ int attn_temporal(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
   return timed(r, K_ATTN, s, 1, [&] { return temporal_attention_launch(a, s); });
 }
 
-int run_block(ddit_req* r, int k, cudaStream_t s) {
+// Self-attention index map of block k (spatial: frames are sequences; temporal: positions).
+ddit_attn self_attn_args(const ddit_req* r, int k) {
   const ddit_config& c = r->m->cfg;
   const Geometry& g = r->g;
   const int C = c.hidden;
-  const bool temporal = k & 1;
-  const int M = temporal ? g.M_tp : g.M_sp;
-  if (M == 0) return DDIT_OK;
-  const int rpb = M / g.B;
-  float* x = temporal ? r->x_tp : r->x_sp;
-  const float* mod = r->mods + (size_t)k * g.B * 6 * C;
-  const GemmPlan* P = &r->plans[(size_t)k * G_N];
-  int rc;
-  if ((rc = ln_mod(r, x, M, mod + 0 * C, mod + 1 * C, rpb, s))) return rc;
-  if ((rc = launch_g(r, P[G_QKV], s))) return rc;
   ddit_attn a;
   memset(&a, 0, sizeof a);
   a.q = r->big;
@@ -357,13 +353,13 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
   a.heads = c.heads;
   a.head_dim = c.head_dim;
   a.scale = 1.0f / std::sqrt((float)c.head_dim);
-  if (!temporal) {  // frames are the sequences: [B*Tl] x S
+  if (!(k & 1)) {
     a.num_seqs = g.B * g.Tl;
     a.Lq = a.Lk = g.S;
     a.q_inner = a.kv_inner = 1;
     a.q_outer = a.kv_outer = g.S;
     a.q_tok = a.kv_tok = 1;
-  } else {  // token positions are the sequences: [B*Sl] x T, stride Sl
+  } else {
     a.num_seqs = g.B * g.Sl;
     a.Lq = a.Lk = g.T;
     a.q_inner = a.kv_inner = g.Sl;
@@ -371,11 +367,18 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
     a.q_inner_stride = a.kv_inner_stride = 1;
     a.q_tok = a.kv_tok = g.Sl;
   }
-  if ((rc = temporal ? attn_temporal(r, &a, s) : attn(r, &a, s))) return rc;
-  if ((rc = launch_g(r, P[G_PROJ], s))) return rc;
-  if ((rc = launch_g(r, P[G_CQ], s))) return rc;
-  // cross attention: each batch's rows attend to its own 300 text tokens
+  return a;
+}
+
+// Cross attention of block k: each batch's rows attend to its own 300 text tokens.
+ddit_attn cross_attn_args(const ddit_req* r, int k) {
+  const ddit_config& c = r->m->cfg;
+  const Geometry& g = r->g;
+  const int C = c.hidden;
+  const int M = (k & 1) ? g.M_tp : g.M_sp;
+  const int rpb = M / g.B;
   const bf16* kv = r->kv + (size_t)k * g.B * c.text_tokens * 2 * C;
+  ddit_attn a;
   memset(&a, 0, sizeof a);
   a.q = r->xm;
   a.ldq = C;
@@ -394,7 +397,63 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
   a.kv_outer = c.text_tokens;
   a.q_tok = a.kv_tok = 1;
   a.scale = 1.0f / std::sqrt((float)c.head_dim);
-  if ((rc = attn(r, &a, s))) return rc;
+  return a;
+}
+
+int build_attn_plans(ddit_req* r) {
+  const int nblk = 2 * r->m->cfg.depth;
+  r->fm_self.assign(nblk, FmhaPlan{});
+  r->fm_cross.assign(nblk, FmhaPlan{});
+  r->fm_self_ok.assign(nblk, 0);
+  r->fm_cross_ok.assign(nblk, 0);
+  for (int k = 0; k < nblk; ++k) {
+    const int M = (k & 1) ? r->g.M_tp : r->g.M_sp;
+    if (M == 0) continue;
+    ddit_attn a = self_attn_args(r, k);
+    if (!(k & 1) && fmha_supported(&a)) {
+      int rc = fmha_plan_init(&r->fm_self[k], &a);
+      if (rc) return rc;
+      r->fm_self_ok[k] = 1;
+    }
+    a = cross_attn_args(r, k);
+    if (fmha_supported(&a)) {
+      int rc = fmha_plan_init(&r->fm_cross[k], &a);
+      if (rc) return rc;
+      r->fm_cross_ok[k] = 1;
+    }
+  }
+  return DDIT_OK;
+}
+
+int run_attn(ddit_req* r, int k, bool cross, cudaStream_t s) {
+  const std::vector<uint8_t>& ok = cross ? r->fm_cross_ok : r->fm_self_ok;
+  if (r->use_tc_attention && ok[k]) {
+    const FmhaPlan& fp = cross ? r->fm_cross[k] : r->fm_self[k];
+    return timed(r, K_ATTN, s, 1, [&] { return fmha_plan_launch(&fp, s); });
+  }
+  ddit_attn a = cross ? cross_attn_args(r, k) : self_attn_args(r, k);
+  if (!cross && (k & 1)) return attn_temporal(r, &a, s);
+  return attn(r, &a, s);
+}
+
+int run_block(ddit_req* r, int k, cudaStream_t s) {
+  const ddit_config& c = r->m->cfg;
+  const Geometry& g = r->g;
+  const int C = c.hidden;
+  const bool temporal = k & 1;
+  const int M = temporal ? g.M_tp : g.M_sp;
+  if (M == 0) return DDIT_OK;
+  const int rpb = M / g.B;
+  float* x = temporal ? r->x_tp : r->x_sp;
+  const float* mod = r->mods + (size_t)k * g.B * 6 * C;
+  const GemmPlan* P = &r->plans[(size_t)k * G_N];
+  int rc;
+  if ((rc = ln_mod(r, x, M, mod + 0 * C, mod + 1 * C, rpb, s))) return rc;
+  if ((rc = launch_g(r, P[G_QKV], s))) return rc;
+  if ((rc = run_attn(r, k, false, s))) return rc;
+  if ((rc = launch_g(r, P[G_PROJ], s))) return rc;
+  if ((rc = launch_g(r, P[G_CQ], s))) return rc;
+  if ((rc = run_attn(r, k, true, s))) return rc;
   if ((rc = launch_g(r, P[G_CPROJ], s))) return rc;
   if ((rc = ln_mod(r, x, M, mod + 3 * C, mod + 4 * C, rpb, s))) return rc;
   if ((rc = launch_g(r, P[G_FC1], s))) return rc;
@@ -602,6 +661,10 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
     delete r;
     return rc == -3 ? DDIT_E_TMA : DDIT_E_INVALID;
   }
+  if ((rc = build_attn_plans(r))) {
+    delete r;
+    return rc;
+  }
   if ((rc = check_cuda("ddit_request_open"))) {
     delete r;
     return rc;
@@ -690,6 +753,16 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->g.P, r->epoch, s); });
   return check_cuda("barrier");
+}
+
+DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value) {
+  switch (option) {
+    case DDIT_OPT_TC_ATTENTION:
+      r->use_tc_attention = value != 0;
+      return DDIT_OK;
+  }
+  set_error("unknown option %d", option);
+  return DDIT_E_INVALID;
 }
 
 DDIT_API int ddit_request_profile(ddit_req* r, int enable) {

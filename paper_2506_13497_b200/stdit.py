@@ -168,6 +168,9 @@ class StepRequest:
                                                   ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def set_option(self, option: int, value: int) -> None:
+        check(lib().ddit_request_set_option(self.handle, option, value))
+
     def profile(self, enable: bool) -> None:
         check(lib().ddit_request_profile(self.handle, 1 if enable else 0))
 

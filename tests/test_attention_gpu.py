@@ -15,8 +15,9 @@ def ref_attn(q, k, v):  # [n, L, H, D]
     return torch.einsum("nhqk,nkhd->nqhd", s.softmax(-1), v.float())
 
 
-@pytest.mark.parametrize("B,T,S", [(2, 3, 405), (2, 1, 64), (1, 2, 130), (2, 4, 1)])
-def test_spatial(cuda, B, T, S):
+@pytest.mark.parametrize("tc", [False, True])
+@pytest.mark.parametrize("B,T,S", [(2, 3, 405), (2, 1, 64), (1, 2, 130), (2, 4, 1), (2, 2, 920), (1, 1, 1620), (1, 3, 256)])
+def test_spatial(cuda, B, T, S, tc):
     from paper_2506_13497_b200 import kernels
     g = torch.Generator().manual_seed(0)
     M = B * T * S
@@ -24,7 +25,7 @@ def test_spatial(cuda, B, T, S):
     o = torch.zeros(M, H * D, device=cuda, dtype=torch.bfloat16)
     C = H * D
     kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=H, num_seqs=B * T,
-                      Lq=S, Lk=S, q_map=(1, S, 0, 1), kv_map=(1, S, 0, 1))
+                      Lq=S, Lk=S, q_map=(1, S, 0, 1), kv_map=(1, S, 0, 1), tc=tc)
     q, k, v = qkv.view(B * T, S, 3, H, D).unbind(2)
     ref = ref_attn(q, k, v).reshape(M, C)
     assert rel_l2(o, ref) < 1e-2
@@ -50,8 +51,9 @@ def test_temporal(cuda, B, T, Sl, fast):
     assert rel_l2(o, ref) < 1e-2
 
 
-@pytest.mark.parametrize("B,N,Ly", [(2, 777, 300), (2, 64, 300), (1, 100, 17)])
-def test_cross(cuda, B, N, Ly):
+@pytest.mark.parametrize("tc", [False, True])
+@pytest.mark.parametrize("B,N,Ly", [(2, 777, 300), (2, 64, 300), (1, 100, 17), (2, 6075, 300)])
+def test_cross(cuda, B, N, Ly, tc):
     from paper_2506_13497_b200 import kernels
     g = torch.Generator().manual_seed(2)
     C = H * D
@@ -59,7 +61,25 @@ def test_cross(cuda, B, N, Ly):
     kv = torch.randn(B * Ly, 2 * C, generator=g).to(cuda, torch.bfloat16)
     o = torch.zeros(B * N, C, device=cuda, dtype=torch.bfloat16)
     kernels.attention(q, kv[:, :C], kv[:, C:], o, heads=H, num_seqs=B, Lq=N, Lk=Ly,
-                      q_map=(1, N, 0, 1), kv_map=(1, Ly, 0, 1))
+                      q_map=(1, N, 0, 1), kv_map=(1, Ly, 0, 1), tc=tc)
     kk, vv = kv.view(B, Ly, 2, H, D).unbind(2)
     ref = ref_attn(q.view(B, N, H, D), kk, vv).reshape(B * N, C)
+    assert rel_l2(o, ref) < 1e-2
+
+
+def test_tc_large_logits_rescale(cuda):
+    """Scores growing along the key axis force the lazy O rescale path."""
+    from paper_2506_13497_b200 import kernels
+    B, T, S = 1, 2, 700
+    C = H * D
+    g = torch.Generator().manual_seed(5)
+    qkv = torch.randn(B * T * S, 3 * C, generator=g)
+    ramp = torch.linspace(0, 6, S).repeat(B * T)[:, None]
+    qkv[:, C:2 * C] *= ramp  # later keys -> much larger logits
+    qkv = qkv.to(cuda, torch.bfloat16)
+    o = torch.zeros(B * T * S, C, device=cuda, dtype=torch.bfloat16)
+    kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=H, num_seqs=B * T,
+                      Lq=S, Lk=S, q_map=(1, S, 0, 1), kv_map=(1, S, 0, 1), tc=True)
+    q, k, v = qkv.view(B * T, S, 3, H, D).unbind(2)
+    ref = ref_attn(q, k, v).reshape(B * T * S, C)
     assert rel_l2(o, ref) < 1e-2

@@ -107,3 +107,22 @@ def test_tiny_step_matches_golden_fixture(cuda, step):
     out = _gpu(cfg, W, sh, z, y, step, cuda)
     ref = g[f"z_{step}"]
     assert rel_l2(out, ref) <= 1e-2 and rel_l2(out - z, ref - z) <= 2e-2
+
+
+def test_tc_and_mma_attention_paths_agree(cuda):
+    """The tcgen05 FMHA (default) and the mma.sync flash kernel give the same step."""
+    from paper_2506_13497_b200 import shapes, weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.XL2, depth=1)
+    W, sh, z, y = _setup(cfg, "240p")
+    model = STDiTModel(cfg, W, cuda)
+    outs = []
+    for tc in (1, 0):
+        req = StepRequest(model, sh, y.to(cuda))
+        req.set_option(1, tc)
+        zd = z.to(cuda).contiguous()
+        req.step(zd, 3)
+        torch.cuda.synchronize()
+        outs.append(zd.cpu())
+    assert rel_l2(outs[0] - z, outs[1] - z) < 5e-3
