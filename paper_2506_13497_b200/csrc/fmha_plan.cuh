@@ -10,6 +10,7 @@ struct FmhaParams {
   int Lq, Lk;
   int q_slot, k_slot, v_slot, o_slot;  // head-slot offsets of head 0 in the maps
   float scale_log2;
+  int q_tiles, heads, seqs;
 };
 
 struct FmhaPlan {

@@ -15,7 +15,10 @@
 //                exp2, lazy O rescaling (only when the running max grows by > 2^8), P written as
 //                bf16 into 128B-swizzled smem (the A operand of PV); final O / l -> bf16 -> smem
 //                -> TMA store.
-// TMEM: S0 [0,128), S1 [128,256), O [256,336) of a 512-column allocation.
+// Persistent: grid = #SMs, each CTA walks work items (q tile fastest); Q, K and V stream through
+// their own double-buffered rings across items, S / P / O are double-buffered, so the epilogue
+// (O / l -> TMA store) of item i overlaps the first tiles of item i+1.
+// TMEM: S0 [0,128), S1 [128,256), O0 [256,336), O1 [384,464) of a 512-column allocation.
 #include "common.cuh"
 #include "ddit.h"
 #include "capi_internal.h"
@@ -28,17 +31,18 @@
 namespace ddit {
 
 namespace fm {
-constexpr int BQ = 128, BKV = 128, THREADS = 256, STAGES = 2;
+constexpr int BQ = 128, BKV = 128, THREADS = 384, KST = 2, VST = 2;
 constexpr int QA = 16384, QB = 4096;                 // Q: 64-col SW128 + 16-col SW32 boxes
 constexpr int KA = 16384, KB = 4096, VA = 16384, VB = 4096;
-constexpr int STAGE = KA + KB + VA + VB;             // 40 KB
 constexpr int PBUF = 2 * 16384;                      // P: two 64-key SW128 regions
-constexpr int OFF_Q = 0;
-constexpr int OFF_KV = QA + QB;                      // 20480 (1024-aligned)
-constexpr int OFF_P = OFF_KV + STAGES * STAGE;       // 102400
-constexpr int OFF_BAR = OFF_P + 2 * PBUF;            // 167936
-constexpr int SMEM = 1024 + OFF_BAR + 256;
-constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O = 256;
+constexpr int OFF_Q = 0;                             // 2 Q buffers
+constexpr int OFF_K = OFF_Q + 2 * (QA + QB);         // KST K stages
+constexpr int OFF_V = OFF_K + KST * (KA + KB);       // VST V stages
+constexpr int OFF_P = OFF_V + VST * (VA + VB);       // 2 P buffers
+constexpr int OFF_OST = OFF_P + 2 * PBUF;            // O staging (128 x 144 B)
+constexpr int OFF_BAR = OFF_OST + 128 * 144;
+constexpr int SMEM = 1024 + OFF_BAR + 26 * 8 + 1024;
+constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
 constexpr float RESCALE_LOG2 = 8.0f;
 }  // namespace fm
 
@@ -120,6 +124,28 @@ DDIT_DEV void st_shared_u4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, ui
                "r"(d)
                : "memory");
 }
+DDIT_DEV void tmem_ld_32x32b_x8_fm(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+// 2^x on the FMA pipe (x <= 0 here): 2^floor(x) * p(frac), p a degree-4 least-squares polynomial of
+// 2^f on [0, 1) (rel. err 5e-6 << bf16), exponent inserted with an integer add.
+DDIT_DEV float poly_exp2(float x) {
+  x = fmaxf(x, -127.f);
+  const float fl = floorf(x);
+  const float f = x - fl;
+  float p = 1.351155e-2f;
+  p = fmaf(p, f, 5.198954e-2f);
+  p = fmaf(p, f, 2.4150888e-1f);
+  p = fmaf(p, f, 6.9297426e-1f);
+  p = fmaf(p, f, 1.00000526f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(fl) << 23));
+}
+DDIT_DEV void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 DDIT_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -138,18 +164,24 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fm_smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [STAGES]
-  uint64_t* kv_empty = bars + 3;  // [STAGES]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;    // [2]
-  uint64_t* pv_done = bars + 11;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_full = bars + 0;    // [2]
+  uint64_t* q_empty = bars + 2;   // [2]
+  uint64_t* k_full = bars + 4;    // [KST]
+  uint64_t* k_empty = bars + 6;   // [KST]
+  uint64_t* v_full = bars + 8;    // [VST]
+  uint64_t* v_empty = bars + 10;  // [VST]
+  uint64_t* s_full = bars + 12;   // [2]
+  uint64_t* s_free = bars + 14;   // [2]
+  uint64_t* p_full = bars + 16;   // [2]
+  uint64_t* pv_done = bars + 18;  // [2]
+  uint64_t* o_full = bars + 20;   // [2]
+  uint64_t* o_free = bars + 22;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  float* xmax = reinterpret_cast<float*>(bars + 26);  // [2][128] partial row maxima / sums
 
   const int warp = warp_id(), lane = lane_id();
-  const int q0 = blockIdx.x * BQ, head = blockIdx.y, seq = blockIdx.z;
   const int nk = (p.Lk + BKV - 1) / BKV;
+  const int n_items = p.q_tiles * p.heads * p.seqs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQa);
@@ -157,16 +189,19 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
     tma_prefetch_desc(&tmKVa);
     tma_prefetch_desc(&tmKVb);
     tma_prefetch_desc(&tmO);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pv_done[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_free[i], 8);
     }
     fence_barrier_init();
   }
@@ -176,167 +211,246 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // work item -> (q tile, head, sequence); q tile fastest so concurrent CTAs share K/V in L2
+  auto decode = [&](int wi, int& qt, int& head, int& seq) {
+    qt = wi % p.q_tiles;
+    head = (wi / p.q_tiles) % p.heads;
+    seq = wi / (p.q_tiles * p.heads);
+  };
+
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
-      mbar_arrive_expect_tx(q_full, QA + QB);
-      tma_load_4d(sm + OFF_Q, &tmQa, q_full, 0, p.q_slot + head, q0, seq);
-      tma_load_4d(sm + OFF_Q + QA, &tmQb, q_full, 64, p.q_slot + head, q0, seq);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % STAGES;
-        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
-        uint8_t* base = sm + OFF_KV + st * STAGE;
-        mbar_arrive_expect_tx(&kv_full[st], STAGE);
-        tma_load_4d(base, &tmKVa, &kv_full[st], 0, p.k_slot + head, j * BKV, seq);
-        tma_load_4d(base + KA, &tmKVb, &kv_full[st], 64, p.k_slot + head, j * BKV, seq);
-        tma_load_4d(base + KA + KB, &tmKVa, &kv_full[st], 0, p.v_slot + head, j * BKV, seq);
-        tma_load_4d(base + KA + KB + VA, &tmKVb, &kv_full[st], 64, p.v_slot + head, j * BKV, seq);
+      int kc = 0, vc = 0, it = 0;
+      for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it) {
+        int qt, head, seq;
+        decode(wi, qt, head, seq);
+        const int qb = it & 1;
+        mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+        uint8_t* qbuf = sm + OFF_Q + qb * (QA + QB);
+        mbar_arrive_expect_tx(&q_full[qb], QA + QB);
+        tma_load_4d(qbuf, &tmQa, &q_full[qb], 0, p.q_slot + head, qt * BQ, seq);
+        tma_load_4d(qbuf + QA, &tmQb, &q_full[qb], 64, p.q_slot + head, qt * BQ, seq);
+        for (int j = 0; j < nk; ++j, ++kc, ++vc) {
+          const int ks = kc % KST, vs = vc % VST;
+          mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
+          uint8_t* kb = sm + OFF_K + ks * (KA + KB);
+          mbar_arrive_expect_tx(&k_full[ks], KA + KB);
+          tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + head, j * BKV, seq);
+          tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + head, j * BKV, seq);
+          mbar_wait(&v_empty[vs], ((vc / VST) & 1) ^ 1);
+          uint8_t* vb = sm + OFF_V + vs * (VA + VB);
+          mbar_arrive_expect_tx(&v_full[vs], VA + VB);
+          tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + head, j * BKV, seq);
+          tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
+        }
       }
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
     constexpr uint32_t id_qk = idesc_f16(128, 128, false);
     constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
     constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
-    const uint32_t qa = smem_u32(sm + OFF_Q), qb = qa + QA;
-    auto issue_qk = [&](int j) {
-      const int st = j % STAGES;
-      const uint32_t ka = smem_u32(sm + OFF_KV + st * STAGE), kb = ka + KA;
-      const uint32_t d = tmem + ((j & 1) ? TM_S1 : TM_S0);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        umma_bf16_ss(d, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2), id_qk, k > 0);
-      umma_bf16_ss(d, sdesc(qb, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
-      umma_commit(&s_full[j & 1]);
-    };
-    mbar_wait(q_full, 0);
-    mbar_wait(&kv_full[0], 0);
-    tc_fence_after();
-    if (elect_one()) issue_qk(0);
-    __syncwarp();
-    for (int j = 0; j < nk; ++j) {
-      if (j + 1 < nk) {
-        const int jn = j + 1;
-        mbar_wait(&kv_full[jn % STAGES], (jn / STAGES) & 1);
-        if (jn >= 2) mbar_wait(&s_free[jn & 1], ((jn - 2) >> 1) & 1);
+    int kc = 0, vc = 0, t0 = 0, it = 0;
+    for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it, t0 += nk) {
+      const int qb = it & 1, ob = it & 1;
+      const uint32_t qa = smem_u32(sm + OFF_Q + qb * (QA + QB)), qbb = qa + QA;
+      const uint32_t o_tm = tmem + (ob ? TM_O1 : TM_O0);
+      mbar_wait(&q_full[qb], (it >> 1) & 1);
+      mbar_wait(&o_free[ob], ((it >> 1) & 1) ^ 1);
+      auto issue_qk = [&](int t) {  // S[t & 1] = Q K^T for global tile t
+        const int ks = kc % KST;
+        mbar_wait(&k_full[ks], (kc / KST) & 1);
+        if (t >= 2) mbar_wait(&s_free[t & 1], ((t - 2) >> 1) & 1);
         tc_fence_after();
-        if (elect_one()) issue_qk(jn);
-        __syncwarp();
-      }
-      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const int st = j % STAGES;
-        const uint32_t va = smem_u32(sm + OFF_KV + st * STAGE + KA + KB), vb = va + VA;
-        const uint32_t pb = smem_u32(sm + OFF_P + (j & 1) * PBUF);
+        if (elect_one()) {
+          const uint32_t ka = smem_u32(sm + OFF_K + ks * (KA + KB)), kb = ka + KA;
+          const uint32_t d = tmem + ((t & 1) ? TM_S1 : TM_S0);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
-          const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
-          umma_bf16_ss(tmem + TM_O, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
-          umma_bf16_ss(tmem + TM_O + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ss(d, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2), id_qk,
+                         k > 0);
+          umma_bf16_ss(d, sdesc(qbb, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
+          umma_commit(&s_full[t & 1]);
+          umma_commit(&k_empty[ks]);
         }
-        umma_commit(&pv_done[j & 1]);
-        umma_commit(&kv_empty[j % STAGES]);
+        __syncwarp();
+        ++kc;
+      };
+      tc_fence_after();
+      issue_qk(t0);
+      for (int j = 0; j < nk; ++j) {
+        const int t = t0 + j;
+        if (j + 1 < nk) issue_qk(t + 1);
+        const int vs = vc % VST;
+        mbar_wait(&p_full[t & 1], (t >> 1) & 1);
+        mbar_wait(&v_full[vs], (vc / VST) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t va = smem_u32(sm + OFF_V + vs * (VA + VB)), vb = va + VA;
+          const uint32_t pb = smem_u32(sm + OFF_P + (t & 1) * PBUF);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+            const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+            umma_bf16_ss(o_tm, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
+            umma_bf16_ss(o_tm + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+          }
+          umma_commit(&pv_done[t & 1]);
+          umma_commit(&v_empty[vs]);
+          if (j == nk - 1) {
+            umma_commit(&q_empty[qb]);
+            umma_commit(&o_full[ob]);
+          }
+        }
+        __syncwarp();
+        ++vc;
       }
-      __syncwarp();
     }
   } else if (warp >= 4) {  // ------------------------------------------ softmax
-    const int ew = warp - 4;
-    const int row = ew * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(ew * 32) << 16);
-    float m = -INFINITY, l = 0.f;
-    int pv_known = -1;  // highest PV index known complete
-    for (int j = 0; j < nk; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+    // 8 warps: warp w covers TMEM lanes 32*(w%4).. (query rows) and key half h = (w-4)/4 of
+    // every S tile (64 of the 128 columns); the two halves of a row exchange their partial
+    // max through smem under a 64-thread named barrier (one per lane quarter).
+    const int quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const int bar_id = 2 + quarter;
+    const bool elected = warp == 4 && lane == 0;
+    int pv_known = -1;  // highest global tile whose PV is known complete
+    int t0 = 0, it = 0;
+    for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it, t0 += nk) {
+      int qt, head, seq;
+      decode(wi, qt, head, seq);
+      const int ob = it & 1;
+      const uint32_t o_tm = lane_base + (ob ? TM_O1 : TM_O0);
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nk; ++j) {
+        const int t = t0 + j;
+        mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+        tc_fence_after();
+        uint32_t s[64];
+        const uint32_t sadr = lane_base + ((t & 1) ? TM_S1 : TM_S0) + half * 64;
+        tmem_ld32(sadr, s);
+        tmem_ld32(sadr + 32, s + 32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[t & 1]);
+        const int valid = min(BKV, p.Lk - j * BKV) - half * 64;  // may be <= 0
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (e < valid) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(s[e]));
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        xmax[half * 128 + row] = mx;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        mx = fmaxf(mx, xmax[(half ^ 1) * 128 + row]);
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float m_new = fmaxf(m, mx * p.scale_log2);
+        const bool resc = m_new > m + RESCALE_LOG2;
+        float alpha = 1.f;
+        if (resc) {
+          alpha = fast_exp2(m - m_new);
+          m = m_new;
+          l *= alpha;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+          if (pv_known < t - 1) {
+            mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+            pv_known = t - 1;
+          }
+          tc_fence_after();
+          if (half == 0) {  // O columns [0, 64)
+            uint32_t o[64];
+            tmem_ld32(o_tm, o);
+            tmem_ld32(o_tm + 32, o + 32);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 64; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(o_tm, o);
+            tmem_st32(o_tm + 32, o + 32);
+          } else {  // O columns [64, 80)
+            uint32_t o[16];
+            tmem_ld16(o_tm + 64, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st16(o_tm + 64, o);
+          }
+          tmem_st_wait();
+        }
+        if (t >= 2 && pv_known < t - 2) {  // P buffer (t & 1) was read by PV_{t-2}
+          mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);
+          pv_known = t - 2;
+        }
+        const uint32_t pbase = smem_u32(sm + OFF_P + (t & 1) * PBUF) + half * 16384;
+        const float neg_m = -m;
+        float rs8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rs8[u] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys (one 128 B swizzled row)
+          float pv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int key = c * 8 + e;
+            const float x = fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m);
+            // balance MUFU and FMA pipes: every 4th exponential by polynomial
+            const float ex = (e & 3) == 3 ? poly_exp2(x) : fast_exp2(x);
+            pv[e] = key < valid ? ex : 0.f;
+            rs8[e] += pv[e];
+          }
+          const uint32_t addr = pbase + (uint32_t)(row * 128 + ((c ^ (row & 7)) << 4));
+          st_shared_u4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
+                       pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+        }
+        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t & 1]);
+      }
+      // ---- item epilogue: O / l -> bf16 -> staging smem (144 B rows) -> TMA store
+      mbar_wait(&o_full[ob], (it >> 1) & 1);
+      pv_known = t0 + nk - 1;
       tc_fence_after();
-      uint32_t s[128];
-      const uint32_t sadr = lane_base + ((j & 1) ? TM_S1 : TM_S0);
-      tmem_ld32(sadr, s);
-      tmem_ld32(sadr + 32, s + 32);
-      tmem_ld32(sadr + 64, s + 64);
-      tmem_ld32(sadr + 96, s + 96);
+      uint32_t o[40];  // half 0: output columns [0, 40), half 1: [40, 72)
+      if (half == 0) {
+        tmem_ld32(o_tm, o);
+        tmem_ld_32x32b_x8_fm(o_tm + 32, o + 32);
+      } else {
+        tmem_ld32(o_tm + 40, o);
+      }
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[j & 1]);
-      const int valid = min(BKV, p.Lk - j * BKV);
-      float mx = -INFINITY;
+      if (lane == 0) mbar_arrive(&o_free[ob]);
+      xmax[half * 128 + row] = l;
+      if (elected) bulk_wait_read0();  // previous item's store no longer reads the staging
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float lt = l + xmax[(half ^ 1) * 128 + row];
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const uint32_t obase = smem_u32(sm + OFF_OST) + row * 144;
+      const int c0 = half ? 5 : 0, nc = half ? 4 : 5;
 #pragma unroll
-      for (int e = 0; e < 128; ++e)
-        if (e < valid) mx = fmaxf(mx, __uint_as_float(s[e]));
-      const float m_new = fmaxf(m, mx * p.scale_log2);
-      const bool resc = m_new > m + RESCALE_LOG2;
-      float alpha = 1.f;
-      if (resc) {
-        alpha = fast_exp2(m - m_new);
-        m = m_new;
-        l *= alpha;
+      for (int c = 0; c < 5; ++c) {
+        if (c < nc)
+          st_shared_u4(obase + (c0 + c) * 16,
+                       pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+                       pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+                       pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+                       pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
       }
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        pv_known = j - 1;
-        tc_fence_after();
-        uint32_t o[80];
-        tmem_ld32(lane_base + TM_O, o);
-        tmem_ld32(lane_base + TM_O + 32, o + 32);
-        tmem_ld16(lane_base + TM_O + 64, o + 64);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 80; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-        tmem_st32(lane_base + TM_O, o);
-        tmem_st32(lane_base + TM_O + 32, o + 32);
-        tmem_st16(lane_base + TM_O + 64, o + 64);
-        tmem_st_wait();
-      }
-      if (j >= 2 && pv_known < j - 2) {  // P buffer (j & 1) was read by PV_{j-2}
-        mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);
-        pv_known = j - 2;
-      }
-      const uint32_t pbase = smem_u32(sm + OFF_P + (j & 1) * PBUF);
-      const float neg_m = -m;
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys
-        float pv[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int key = c * 8 + e;
-          pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
-          rs += pv[e];
-        }
-        const uint32_t addr = pbase + (c >> 3) * 16384 + (uint32_t)(row * 128 + (((c & 7) ^ (row & 7)) << 4));
-        st_shared_u4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
-                     pack_bf16(pv[6], pv[7]));
-      }
-      l += rs;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // staging written; xmax reusable
+      if (elected) {
+        tma_store_4d(&tmO, sm + OFF_OST, 0, p.o_slot + head, qt * BQ, seq);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     }
-    // ---- epilogue: O / l -> bf16 -> smem (144 B rows) -> TMA store (clipped at Lq)
-    mbar_wait(&pv_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
-    tc_fence_after();
-    uint32_t o[80];
-    tmem_ld32(lane_base + TM_O, o);
-    tmem_ld32(lane_base + TM_O + 32, o + 32);
-    tmem_ld16(lane_base + TM_O + 64, o + 64);
-    tmem_ld_wait();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const uint32_t obase = smem_u32(sm + OFF_P) + row * 144;
-#pragma unroll
-    for (int c = 0; c < 9; ++c)
-      st_shared_u4(obase + c * 16,
-                   pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
-                   pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
-                   pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
-                   pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (ew == 0 && lane == 0) {
-      tma_store_4d(&tmO, sm + OFF_P, 0, p.o_slot + head, q0, seq);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
+    if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -426,7 +540,14 @@ int fmha_plan_init(FmhaPlan* fp, const ddit_attn* a) {
   fp->p.v_slot = v_slot;
   fp->p.o_slot = 0;
   fp->p.scale_log2 = a->scale * 1.4426950408889634f;
-  fp->grid = dim3((a->Lq + fm::BQ - 1) / fm::BQ, a->heads, a->num_seqs);
+  fp->p.q_tiles = (a->Lq + fm::BQ - 1) / fm::BQ;
+  fp->p.heads = a->heads;
+  fp->p.seqs = a->num_seqs;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int items = fp->p.q_tiles * a->heads * a->num_seqs;
+  fp->grid = dim3(items < sms ? items : sms, 1, 1);
   return DDIT_OK;
 }
 
