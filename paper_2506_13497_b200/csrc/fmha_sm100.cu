@@ -143,6 +143,25 @@ DDIT_DEV float poly_exp2(float x) {
   p = fmaf(p, f, 1.00000526f);
   return __int_as_float(__float_as_int(p) + (static_cast<int>(fl) << 23));
 }
+// Blackwell packed fp32: two FMAs / adds per instruction, and a 3-input max.
+DDIT_DEV void ffma2(float& d0, float& d1, float a0, float a1, float b, float c) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %5};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+DDIT_DEV void fadd2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+      "add.rn.f32x2 ra, ra, rb;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
+DDIT_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 DDIT_DEV void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -339,9 +358,16 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         float mx8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+        const bool full = valid >= 64;  // every tile but the ragged last one
+        if (full) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          if (e < valid) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(s[e]));
+          for (int e = 0; e < 64; e += 2)
+            mx8[(e >> 1) & 7] = fmax3(mx8[(e >> 1) & 7], __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e < valid) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(s[e]));
+        }
         float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         xmax[half * 128 + row] = mx;
@@ -390,21 +416,36 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         float rs8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) rs8[u] = 0.f;
+        const uint32_t prow = pbase + (uint32_t)(row * 128);
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys (one 128 B swizzled row)
-          float pv[8];
+          for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys (one 128 B swizzled row)
+            float pv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int key = c * 8 + e;
-            const float x = fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m);
-            // balance MUFU and FMA pipes: every 4th exponential by polynomial
-            const float ex = (e & 3) == 3 ? poly_exp2(x) : fast_exp2(x);
-            pv[e] = key < valid ? ex : 0.f;
-            rs8[e] += pv[e];
+            for (int e = 0; e < 8; e += 2) {
+              float x0, x1;
+              ffma2(x0, x1, __uint_as_float(s[c * 8 + e]), __uint_as_float(s[c * 8 + e + 1]),
+                    p.scale_log2, neg_m);
+              pv[e] = fast_exp2(x0);
+              pv[e + 1] = fast_exp2(x1);
+              fadd2(rs8[e], rs8[e + 1], pv[e], pv[e + 1]);
+            }
+            st_shared_u4(prow + ((c ^ (row & 7)) << 4), pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
+                         pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
           }
-          const uint32_t addr = pbase + (uint32_t)(row * 128 + ((c ^ (row & 7)) << 4));
-          st_shared_u4(addr, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
-                       pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float pv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int key = c * 8 + e;
+              pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
+              rs8[e] += pv[e];
+            }
+            st_shared_u4(prow + ((c ^ (row & 7)) << 4), pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
+                         pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+          }
         }
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
