@@ -38,6 +38,9 @@ extern "C" {
 DDIT_API const char* ddit_last_error(void);
 DDIT_API int ddit_version(void);
 DDIT_API int ddit_num_sms(void);
+/* GEMM kernel selection for plans built afterwards: 1 (default) = cta_group::2 kernel
+ * (256-row tiles over a CTA pair), 0 = single-CTA kernel (128-row tiles). Env DDIT_GEMM_2CTA=0. */
+DDIT_API int ddit_set_gemm_2cta(int on);
 
 /* ------------------------------------------------------------------ kernel-level ops
  * Exposed for parity tests and profiling; the step below composes them. */

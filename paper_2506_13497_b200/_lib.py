@@ -117,6 +117,7 @@ class Attn(ctypes.Structure):
 
 
 _SIGNATURES = {
+    "ddit_set_gemm_2cta": [ci],
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
     "ddit_attention_tc": [ctypes.POINTER(Attn), vp],

@@ -56,6 +56,10 @@ extern "C" {
 DDIT_API const char* ddit_last_error(void) { return g_capi_err; }
 DDIT_API int ddit_version(void) { return 1; }
 DDIT_API int ddit_num_sms(void) { return num_sms(); }
+DDIT_API int ddit_set_gemm_2cta(int on) {
+  set_two_cta(on);
+  return DDIT_OK;
+}
 
 DDIT_API int ddit_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int epi,
                        const ddit_epi* ep, int bn, void* stream) {

@@ -17,6 +17,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 namespace ddit {
@@ -120,13 +121,32 @@ DDIT_DEV float gelu_fast(float x) {
 struct EpiCtx {
   int m_tiles, n_tiles, num_tiles;
   int M;
+  int next_m0, next_n0;  // this CTA's next tile (residual prefetch), next_m0 < 0: none
 };
+
+DDIT_DEV void mbar_arrive_cl(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
+               : "memory");
+}
+DDIT_DEV uint32_t cluster_addr(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+DDIT_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DDIT_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // ------------------------------------------------------------------ epilogue: bf16 / gelu / f32
 template <int BN, int EPI>
 DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
                              uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
-                             uint64_t* tempty_bar, int lane) {
+                             uint32_t tempty_cl, int lane) {
   constexpr int SUB = EpiCfg<BN, EPI>::SUB;
   constexpr int NS = BN / SUB;
 #pragma unroll 1
@@ -142,7 +162,7 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
     if (sub == NS - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar);
+      if (lane == 0) mbar_arrive_cl(tempty_cl);
     }
     const int col0 = n0 + sub * SUB;
     float v[SUB];
@@ -190,33 +210,18 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
 // ------------------------------------------------------------------ epilogue: gated residual
 // x[r, c] += gate[b(r), c] * (acc + bias[c]) in fp32 through TMA (load, update in smem, store),
 // plus an optional bf16 copy of the new x (the cross-attention query input).
-template <int BN>
+// Coordinates of the residual sub-tile after (this tile, sub): the next sub-tile of the same
+// tile, else sub-tile 0 of this CTA's next tile (m_next < 0: none).
 struct ResidNext {
   int m0, n0, sub;
   bool valid;
 };
 
 template <int BN>
-DDIT_DEV ResidNext<BN> resid_next(int tile, int sub, int n_tiles, int num_tiles) {
-  constexpr int NS = BN / 32;
-  ResidNext<BN> n;
-  if (sub + 1 < NS) {
-    n.sub = sub + 1;
-  } else {
-    n.sub = 0;
-    tile += gridDim.x;
-  }
-  n.valid = tile < num_tiles;
-  n.m0 = (tile / n_tiles) * BM;
-  n.n0 = (tile % n_tiles) * BN;
-  return n;
-}
-
-template <int BN>
 DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const CUtensorMap* tmO2,
-                             uint8_t* sE, uint64_t* rbar, uint32_t taddr, int rit, int tile,
+                             uint8_t* sE, uint64_t* rbar, uint32_t taddr, int rit,
                              int m0, int n0, const EpiCtx& cx, bool elected, int& cnt,
-                             uint64_t* tempty_bar, int lane) {
+                             uint32_t tempty_cl, int lane) {
   constexpr int NS = BN / 32;
   const int row = m0 + rit;
   const int grow = row < cx.M ? row : cx.M - 1;
@@ -228,7 +233,18 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
     uint8_t* ob = sE + 2 * 16384 + buf * 8192;
     if (elected) {
       bulk_wait_read<0>();  // buffer buf^1 (previous sub-tile) no longer read by its stores
-      ResidNext<BN> nx = resid_next<BN>(tile, sub, cx.n_tiles, cx.num_tiles);
+      ResidNext nx;
+      if (sub + 1 < NS) {
+        nx.valid = true;
+        nx.m0 = m0;
+        nx.n0 = n0;
+        nx.sub = sub + 1;
+      } else {
+        nx.valid = cx.next_m0 >= 0;
+        nx.m0 = cx.next_m0;
+        nx.n0 = cx.next_n0;
+        nx.sub = 0;
+      }
       if (nx.valid) {
         mbar_arrive_expect_tx(&rbar[buf ^ 1], 16384);
         tma_load_2d(sE + (buf ^ 1) * 16384, tmR, &rbar[buf ^ 1], nx.n0 + nx.sub * 32, nx.m0);
@@ -241,7 +257,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
     if (sub == NS - 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar);
+      if (lane == 0) mbar_arrive_cl(tempty_cl);
     }
     const int col0 = n0 + sub * 32;
     const uint32_t rbase = smem_u32(rb);
@@ -285,7 +301,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
 // q,k: bias -> per-head RMSNorm (weight) -> optional interleaved RoPE by frame index.
 DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
                            uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
-                           uint64_t* tempty_bar, int lane) {
+                           uint32_t tempty_cl, int lane) {
   constexpr int HD = 72;
   const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
   const int row = m0 + rit;
@@ -304,7 +320,7 @@ DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t*
     if (h == 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar);
+      if (lane == 0) mbar_arrive_cl(tempty_cl);
     }
     const int c0 = n0 + h * HD;
     float v[72];
@@ -486,16 +502,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m0 = (tile / n_tiles) * BM;
       const int n0 = (tile % n_tiles) * BN;
+      const int nt = tile + gridDim.x;
+      cx.next_m0 = nt < num_tiles ? (nt / n_tiles) * BM : -1;
+      cx.next_n0 = nt < num_tiles ? (nt % n_tiles) * BN : 0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
+      const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
-        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, &tempty[acc], lane);
+        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       } else if constexpr (EPI == EPI_RESID) {
-        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, tile, m0, n0, cx, elected, cnt,
-                           &tempty[acc], lane);
+        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, m0, n0, cx, elected, cnt, tcl,
+                           lane);
       } else {
-        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, &tempty[acc], lane);
+        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -507,6 +527,217 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ 2-CTA kernel
+// cta_group::2: a cluster of two CTAs (one TPC) computes a 256 x BN tile. CTA r holds rows
+// [128r, 128r+128) of A and rows [r*BN/2, (r+1)*BN/2) of B in its smem and the accumulator rows
+// [128r, 128r+128) x BN in its TMEM; the leader (rank 0) issues tcgen05.mma.cta_group::2 with
+// M = 256. Each SM streams half the B operand of the 1-CTA kernel.
+template <int BN, int EPI>
+struct GemmCfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int BUDGET = 232448 - 1024 - BAR_BYTES - EpiCfg<BN, EPI>::BYTES;
+  static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EpiCfg<BN, EPI>::BYTES + BAR_BYTES;
+  static_assert(B_BYTES % 1024 == 0, "B half-tile must keep 1024 B swizzle-atom alignment");
+  static_assert(BN % 16 == 0 && (BN / 2) % 8 == 0 && BN <= 256, "invalid UMMA N for cta_group::2");
+  static_assert(STAGES >= 3, "pipeline too shallow");
+};
+
+DDIT_DEV void tma_load_2d_cg2(void* smem_dst, const void* tmap, uint32_t bar_leader, int c0, int c1,
+                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+DDIT_DEV void umma_bf16_ss_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+DDIT_DEV void umma_commit_cg2_mc(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmO,
+                         const __grid_constant__ CUtensorMap tmR,
+                         const __grid_constant__ CUtensorMap tmO2, int M, int N, int K,
+                         const __grid_constant__ EpiParams ep) {
+  using Cfg = GemmCfg2<BN, EPI>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int BM2 = 2 * BM;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + EpiCfg<BN, EPI>::BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  EpiCtx cx;
+  cx.M = M;
+  cx.m_tiles = (M + BM2 - 1) / BM2;
+  cx.n_tiles = N / BN;
+  cx.num_tiles = cx.m_tiles * cx.n_tiles;
+  const int n_tiles = cx.n_tiles;
+  const int num_tiles = cx.num_tiles;
+  const int k_blocks = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmO);
+    if constexpr (EPI == EPI_RESID) tma_prefetch_desc(&tmR);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&rbar[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---- producer (both CTAs): own halves of A and B -> leader's barrier
+      const uint64_t pol_a = l2_policy_evict_first();
+      const uint64_t pol_b = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += nclusters) {
+        const int m0 = (tile / n_tiles) * BM2 + rank * BM;
+        const int nb0 = (tile % n_tiles) * BN + rank * (BN / 2);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          const uint32_t bar0 = cluster_addr(&full[stage], 0);
+          tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, bar0, kb * BK, m0, pol_a);
+          tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, bar0, kb * BK, nb0, pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // ---- MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = make_idesc_bf16(BM2, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += nclusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccStride;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_ss_cg2(d_tmem, make_sdesc_sw128(a_base + k * 32),
+                               make_sdesc_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+            umma_commit_cg2_mc(&empty[stage]);
+            if (kb == k_blocks - 1) umma_commit_cg2_mc(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue (both CTAs): own 128 accumulator rows
+    const int ew = warp - 4;
+    const int rit = ew * 32 + lane;
+    const bool elected = (ew == 0 && lane == 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int cnt = 0;
+    if constexpr (EPI == EPI_RESID) {
+      if (elected && cid < num_tiles) {
+        mbar_arrive_expect_tx(&rbar[0], 16384);
+        tma_load_2d(sE, &tmR, &rbar[0], (cid % n_tiles) * BN, (cid / n_tiles) * BM2 + rank * BM);
+      }
+    }
+    for (int tile = cid; tile < num_tiles; tile += nclusters) {
+      const int m0 = (tile / n_tiles) * BM2 + rank * BM;
+      const int n0 = (tile % n_tiles) * BN;
+      const int nt = tile + nclusters;
+      cx.next_m0 = nt < num_tiles ? (nt / n_tiles) * BM2 + rank * BM : -1;
+      cx.next_n0 = nt < num_tiles ? (nt % n_tiles) * BN : 0;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
+      const uint32_t tcl = cluster_addr(&tempty[acc], 0);
+      if constexpr (EPI == EPI_QKV) {
+        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+      } else if constexpr (EPI == EPI_RESID) {
+        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, m0, n0, cx, elected, cnt, tcl,
+                           lane);
+      } else {
+        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (elected) bulk_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(kTmemCols)
+                 : "memory");
   }
 }
 
@@ -595,10 +826,12 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
     return -2;
   }
   memset(p, 0, sizeof *p);
+  p->two_cta = two_cta_enabled() ? 1 : 0;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   if (make_tmap(&p->tmA, A, BF, 2, M, K, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;
-  if (make_tmap(&p->tmB, B, BF, 2, N, K, ldb, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;
+  const int bbox = p->two_cta ? bn / 2 : bn;
+  if (make_tmap(&p->tmB, B, BF, 2, N, K, ldb, bbox, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;
   switch (epi) {
     case EPI_BF16:
     case EPI_GELU_BF16: {
@@ -636,13 +869,53 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
   p->bn = bn;
   p->epi = epi;
   p->ep = ep;
-  const int tiles = ((M + BM - 1) / BM) * (N / bn);
-  p->grid = tiles < num_sms() ? tiles : num_sms();
+  if (p->two_cta) {
+    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / bn);
+    const int clusters = num_sms() / 2;
+    p->grid = 2 * (tiles < clusters ? tiles : clusters);
+  } else {
+    const int tiles = ((M + BM - 1) / BM) * (N / bn);
+    p->grid = tiles < num_sms() ? tiles : num_sms();
+  }
+  return 0;
+}
+
+static int g_two_cta = -1;
+bool two_cta_enabled() {
+  if (g_two_cta < 0) {
+    const char* e = getenv("DDIT_GEMM_2CTA");
+    g_two_cta = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_two_cta != 0;
+}
+void set_two_cta(int on) { g_two_cta = on ? 1 : 0; }
+
+template <int BN, int EPI>
+static int launch_t2(const GemmPlan* p, cudaStream_t s) {
+  constexpr int smem = GemmCfg2<BN, EPI>::SMEM;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm2_bf16_tn_kernel<BN, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) {
+      snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return -4;
+    }
+    attr_set = true;
+  }
+  gemm2_bf16_tn_kernel<BN, EPI><<<p->grid, kThreads, smem, s>>>(p->tmA, p->tmB, p->tmO, p->tmR,
+                                                                 p->tmO2, p->M, p->N, p->K, p->ep);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof g_err, "gemm2 launch: %s", cudaGetErrorString(e));
+    return -4;
+  }
   return 0;
 }
 
 template <int BN, int EPI>
 static int launch_t(const GemmPlan* p, cudaStream_t s) {
+  if (p->two_cta) return launch_t2<BN, EPI>(p, s);
   constexpr int smem = GemmCfg<BN, EPI>::SMEM;
   static bool attr_set = false;
   if (!attr_set) {

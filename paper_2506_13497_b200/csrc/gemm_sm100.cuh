@@ -50,6 +50,7 @@ struct GemmPlan {
   int epi;
   EpiParams ep;
   int grid;
+  int two_cta;  // 1: cta_group::2 kernel (M = 256 tiles over a CTA pair)
 };
 
 // Build the TMA descriptors and launch geometry. Returns 0 on success.
@@ -57,6 +58,8 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
                    int K, int epi, const EpiParams& ep, int bn);
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
 int num_sms();
+bool two_cta_enabled();
+void set_two_cta(int on);
 const char* gemm_last_error();
 
 }  // namespace ddit

@@ -7,6 +7,15 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=[1, 0], ids=["2cta", "1cta"], autouse=True)
+def gemm_mode(request, cuda):
+    from paper_2506_13497_b200 import _lib
+
+    _lib.lib().ddit_set_gemm_2cta(request.param)
+    yield request.param
+    _lib.lib().ddit_set_gemm_2cta(1)
+
+
 def rel_l2(a, b):
     a = a.float()
     b = b.float()
