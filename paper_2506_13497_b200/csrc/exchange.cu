@@ -16,9 +16,11 @@ namespace ddit {
 DDIT_DEV void signal_peers(const ExchangeSync& sync) {
   // called by one thread of the last CTA
   __threadfence_system();
+  const uint32_t e = *sync.epoch + 1;
+  *sync.epoch = e;
   for (int q = 0; q < sync.P; ++q) {
     uint32_t* remote = sync.flags.p[q] + sync.rank;
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(sync.epoch) : "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(e) : "memory");
   }
 }
 
@@ -105,10 +107,11 @@ int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S
   return 1;
 }
 
-// Wait until every rank q published `epoch` into this rank's slot q.
-__global__ void flag_wait_kernel(const uint32_t* flags, int P, uint32_t epoch) {
+// Wait until every rank q published this rank's current epoch into slot q.
+__global__ void flag_wait_kernel(const uint32_t* flags, const uint32_t* epoch_p, int P) {
   const int q = threadIdx.x;
   if (q >= P) return;
+  const uint32_t epoch = *epoch_p;
   const uint32_t* mine = flags + q;
   uint32_t v;
   do {
@@ -116,8 +119,8 @@ __global__ void flag_wait_kernel(const uint32_t* flags, int P, uint32_t epoch) {
   } while ((int32_t)(v - epoch) < 0);
 }
 
-int flag_wait(const uint32_t* own_flags, int P, uint32_t epoch, cudaStream_t s) {
-  flag_wait_kernel<<<1, 32, 0, s>>>(own_flags, P, epoch);
+int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, cudaStream_t s) {
+  flag_wait_kernel<<<1, 32, 0, s>>>(own_flags, epoch, P);
   return 1;
 }
 

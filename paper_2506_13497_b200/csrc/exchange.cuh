@@ -13,16 +13,18 @@ struct PeerFlags {
 };
 // Completion signalling of one exchange: flags.p[q] = rank q's flag array (uint32 [P]),
 // counter = this rank's CTA ticket counter (device, zero-initialised).
+// The epoch lives in device memory (incremented by the last CTA of every exchange), so a
+// captured CUDA graph of the step stays correct on every replay.
 struct ExchangeSync {
   PeerFlags flags;  // p[0] == nullptr: no signalling (virtual ranks, stream-ordered)
   unsigned int* counter;
+  uint32_t* epoch;  // this rank's exchange counter
   int rank, P;
-  uint32_t epoch;
 };
 // Return the number of kernels launched (0 or 1).
 int exchange_sp_to_tp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
                       int t_lo, int Tl, const ExchangeSync& sync, cudaStream_t s);
 int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
                       int s_lo, int Sl, const ExchangeSync& sync, cudaStream_t s);
-int flag_wait(const uint32_t* own_flags, int P, uint32_t epoch, cudaStream_t s);
+int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, cudaStream_t s);
 }  // namespace ddit

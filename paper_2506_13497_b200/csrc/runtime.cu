@@ -152,7 +152,6 @@ struct ddit_req {
   bool peers_set = false;
   bool flags_set = false;
   bool use_tc_attention = true;  // tcgen05 FMHA for spatial / cross attention
-  uint32_t epoch = 0;
   // profiling: event pairs around every launch, tagged by kernel class
   bool prof_on = false;
   std::vector<cudaEvent_t> ev;
@@ -474,9 +473,9 @@ int push_exchange(ddit_req* r, int k, cudaStream_t s) {
   if (r->flags_set) {
     sync.flags = r->peer_flags;
     sync.counter = r->counter;
+    sync.epoch = r->counter + 1;
     sync.rank = g.rank;
     sync.P = g.P;
-    sync.epoch = ++r->epoch;
   }
   int n = 0;
   timed(r, K_EXCH, s, 0, [&] {
@@ -751,7 +750,7 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
     return DDIT_E_CONFIG;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->g.P, r->epoch, s); });
+  timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->counter + 1, r->g.P, s); });
   return check_cuda("barrier");
 }
 

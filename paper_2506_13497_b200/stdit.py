@@ -152,6 +152,24 @@ class StepRequest:
         check(lib().ddit_dit_step(self.handle, z_local.data_ptr(), step, stream_ptr(stream)))
         return z_local
 
+    def graph_step(self, z_local: torch.Tensor, step: int) -> torch.Tensor:
+        """The same step replayed from a CUDA graph (captured on first use per step index and
+        latent buffer): the ~570 kernel launches of a step become one graph launch."""
+        key = (step, z_local.data_ptr())
+        graphs = self.__dict__.setdefault("_graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            scratch = torch.empty_like(z_local)
+            scratch.copy_(z_local)
+            with torch.cuda.graph(g):
+                self.step(z_local, step)
+            z_local.copy_(scratch)  # capture does not execute; keep the caller's latent intact
+            graphs[key] = g
+        g.replay()
+        return z_local
+
     # phase API (virtual ranks in lockstep on one device)
     def begin(self, z_local, step, stream=None):
         check(lib().ddit_step_begin(self.handle, z_local.data_ptr(), step, stream_ptr(stream)))

@@ -30,6 +30,8 @@ g = GroupStep(model, sh, y.to(dev))
 zl = z[:, :, g.shard.t_lo:g.shard.t_hi].to(dev).contiguous()
 for step in (0, 1):
     g.step(zl, step)
+for step in (2, 3):  # CUDA-graph replays: the device-side exchange epoch must advance
+    g.req.graph_step(zl, step)
 torch.cuda.synchronize()
 parts = [None] * world
 dist.all_gather_object(parts, zl.cpu())
@@ -37,7 +39,7 @@ ok = True
 if rank == 0:
     z1 = z.to(dev).contiguous()
     req = StepRequest(model, sh, y.to(dev))
-    for step in (0, 1):
+    for step in (0, 1, 2, 3):
         req.step(z1, step)
     torch.cuda.synchronize()
     zp = torch.cat(parts, dim=2)

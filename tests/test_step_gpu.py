@@ -126,3 +126,20 @@ def test_tc_and_mma_attention_paths_agree(cuda):
         torch.cuda.synchronize()
         outs.append(zd.cpu())
     assert rel_l2(outs[0] - z, outs[1] - z) < 5e-3
+
+
+def test_graph_replay_matches_eager(cuda):
+    from paper_2506_13497_b200 import weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = weights.TINY
+    W, sh, z, y = _setup(cfg, "144p-16f")
+    model = STDiTModel(cfg, W, cuda)
+    req = StepRequest(model, sh, y.to(cuda))
+    z1 = z.to(cuda).contiguous()
+    z2 = z.to(cuda).contiguous()
+    for step in (0, 1, 2):
+        req.step(z1, step)
+        req.graph_step(z2, step)
+    torch.cuda.synchronize()
+    assert torch.equal(z1, z2)
