@@ -41,6 +41,8 @@ DDIT_API int ddit_num_sms(void);
 /* GEMM kernel selection for plans built afterwards: 1 (default) = cta_group::2 kernel
  * (256-row tiles over a CTA pair), 0 = single-CTA kernel (128-row tiles). Env DDIT_GEMM_2CTA=0. */
 DDIT_API int ddit_set_gemm_2cta(int on);
+/* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */
+DDIT_API int ddit_enable_peer_access(int device, int peer);
 
 /* ------------------------------------------------------------------ kernel-level ops
  * Exposed for parity tests and profiling; the step below composes them. */
@@ -220,6 +222,15 @@ DDIT_API int ddit_request_profile(ddit_req* r, int enable);
 DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count);
 /* Total kernel launches issued by libddit in this process. */
 DDIT_API unsigned long long ddit_launch_count(void);
+
+/* ------------------------------------------------------------------ re-sharding (K11 / K12)
+ * dst (fp32 [channels][t_hi-t_lo][hw], this rank's new T-shard) <- frames gathered from up to
+ * 16 source shards src[k] ([channels][src_t_hi[k]-src_t_lo[k]][hw], peer or local pointers).
+ * Promotion P -> P' (reference engine.py:281-290) and the DiT -> VAE hand-off to the vae_dop
+ * lowest-id GPUs (policies.py:175-190) are both this gather. */
+DDIT_API int ddit_latent_gather(float* dst, int t_lo, int t_hi, const float* const* src,
+                                const int* src_t_lo, const int* src_t_hi, int nsrc, int channels,
+                                int hw, void* stream);
 
 /* ------------------------------------------------------------------ cross-process mapping
  * One process per GPU: a rank exports the (allocation handle, offset) of its exchange buffers

@@ -118,6 +118,7 @@ class Attn(ctypes.Structure):
 
 _SIGNATURES = {
     "ddit_set_gemm_2cta": [ci],
+    "ddit_enable_peer_access": [ci, ci],
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
     "ddit_attention_tc": [ctypes.POINTER(Attn), vp],
@@ -137,6 +138,8 @@ _SIGNATURES = {
     "ddit_request_profile": [vp, ci],
     "ddit_request_set_option": [vp, ci, ci],
     "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
+    "ddit_latent_gather": [vp, ci, ci, ctypes.POINTER(vp), ctypes.POINTER(ci), ctypes.POINTER(ci),
+                           ci, ci, ci, vp],
     "ddit_ipc_export": [vp, vp, ctypes.POINTER(ctypes.c_uint64)],
     "ddit_ipc_import": [vp, ctypes.c_uint64, ctypes.POINTER(vp)],
     "ddit_ipc_close": [vp, ctypes.c_uint64],

@@ -56,6 +56,22 @@ extern "C" {
 DDIT_API const char* ddit_last_error(void) { return g_capi_err; }
 DDIT_API int ddit_version(void) { return 1; }
 DDIT_API int ddit_num_sms(void) { return num_sms(); }
+DDIT_API int ddit_enable_peer_access(int device, int peer) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(cur);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return DDIT_OK;
+  }
+  if (e != cudaSuccess) {
+    set_error("cudaDeviceEnablePeerAccess(%d -> %d): %s", device, peer, cudaGetErrorString(e));
+    return DDIT_E_CUDA;
+  }
+  return DDIT_OK;
+}
 DDIT_API int ddit_set_gemm_2cta(int on) {
   set_two_cta(on);
   return DDIT_OK;

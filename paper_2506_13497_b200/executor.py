@@ -1,0 +1,231 @@
+"""Real B200 work behind the serving loop's step sites, and the measured profile.
+
+``B200Executor`` implements ``sched.StepExecutor``: plugged into ``sched.Simulation(...,
+executor=...)`` it runs the actual STDiT3 step wherever the reference only looks a time up --
+DiT step at start (reference pkg/src/ditsim/engine.py:245), after a promotion (:289), steady
+state (:292) -- and the DiT->VAE hand-off before the VAE (:305). The engine's clock advances by
+the measured (CUDA-event) durations, so traces are driven by real step times while every
+allocator / policy decision stays the reference's.
+
+* A request's latent lives as per-rank T-shards on the GPUs of its group. On a promotion
+  P -> P' (the engine jumps from the applied set to the final pending set, SURVEY Appendix
+  A.6) the new group's ranks gather their new frame ranges from the old shards with
+  ``ddit_latent_gather`` (peer loads) before the step -- the reference's 1 ms + 1 ms constants
+  (engine.py:52-61) become a measured re-shard.
+* Engine GPU ids map onto physical devices ``gpu_id % device_count``. A group whose ids all
+  land on one device runs as virtual ranks in lockstep (``VirtualGroup``); a group spanning
+  devices runs one rank per device concurrently with the peer-store exchange.
+* ``profile_b200`` measures ``dit_step_seconds`` per (resolution, DoP) and emits the
+  reference's ``dit-profile/1`` document (profiles.py:132-215).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from ._lib import check, lib
+from .shapes import VideoShape, shape_of
+from .sched.engine import RequestState
+from .stdit import STDiTModel, StepRequest, VirtualGroup
+from .weights import STDiTConfig, synthetic_inputs
+
+vp, ci = ctypes.c_void_p, ctypes.c_int
+
+
+def latent_gather(dst: torch.Tensor, t_lo: int, t_hi: int, sources: list[tuple[torch.Tensor, int, int]],
+                  stream=None) -> None:
+    """dst [1|., C, t_hi-t_lo, H, W] <- frames of the shards (tensor, t_lo, t_hi) that cover it."""
+    from ._lib import stream_ptr
+
+    n = len(sources)
+    P = (vp * n)(*[s[0].data_ptr() for s in sources])
+    lo = (ci * n)(*[s[1] for s in sources])
+    hi = (ci * n)(*[s[2] for s in sources])
+    C, HW = dst.shape[-4], dst.shape[-2] * dst.shape[-1]
+    check(lib().ddit_latent_gather(dst.data_ptr(), t_lo, t_hi, P, lo, hi, n, C, HW, stream_ptr(stream)))
+
+
+@dataclass
+class _Live:
+    """One request's device state on its current group."""
+
+    gpu_ids: tuple[int, ...]
+    ranks: list[StepRequest]
+    shards: list[torch.Tensor]  # z T-shards, rank order
+    group: VirtualGroup | None = None
+    steps_done: int = 0
+    history: list[tuple[int, ...]] = field(default_factory=list)
+
+
+class B200Executor:
+    """Executes real STDiT3 steps for ``sched.Simulation`` (see module docstring)."""
+
+    def __init__(self, cfg: STDiTConfig, weights: dict[str, torch.Tensor], *,
+                 shapes: dict[str, VideoShape] | None = None, num_steps: int = 30,
+                 guidance: float = 7.0, seed_base: int = 0):
+        self.cfg = cfg
+        self.ndev = max(torch.cuda.device_count(), 1)
+        self.models: dict[int, STDiTModel] = {}
+        self._weights = weights
+        self.shapes = shapes or {}
+        self.num_steps = num_steps
+        self.guidance = guidance
+        self.seed_base = seed_base
+        self.live: dict[int, _Live] = {}
+        self.final_latents: dict[int, torch.Tensor] = {}
+        self.step_seconds: list[tuple[int, int, float]] = []  # (request, dop, seconds)
+        self.reshard_seconds: list[float] = []
+
+    # ---------------------------------------------------------------- helpers
+    def device_of(self, gpu_id: int) -> int:
+        return gpu_id % self.ndev
+
+    def _model(self, dev: int) -> STDiTModel:
+        if dev not in self.models:
+            self.models[dev] = STDiTModel(self.cfg, self._weights, torch.device("cuda", dev))
+        return self.models[dev]
+
+    def _shape(self, request: RequestState) -> VideoShape:
+        return self.shapes.get(request.resolution) or shape_of(request.resolution)
+
+    def _inputs(self, request: RequestState):
+        sh = self._shape(request)
+        return synthetic_inputs(self.cfg, sh.latent, seed_z=self.seed_base + 2 * request.request_id,
+                                seed_y=self.seed_base + 2 * request.request_id + 1)
+
+    def _open(self, request: RequestState, gpu_ids: tuple[int, ...]) -> _Live:
+        sh = self._shape(request)
+        _, y = self._inputs(request)
+        devs = [self.device_of(g) for g in gpu_ids]
+        dop = len(gpu_ids)
+        if len(set(devs)) == 1:
+            model = self._model(devs[0])
+            with torch.cuda.device(devs[0]):
+                grp = VirtualGroup(model, sh, y.to(model.device), dop, num_steps=self.num_steps,
+                                   guidance=self.guidance)
+            ranks, group = grp.ranks, grp
+        else:
+            if len(set(devs)) != dop:
+                raise RuntimeError(f"group {gpu_ids} maps several ranks onto one device of many")
+            ranks = []
+            for r, d in enumerate(devs):
+                with torch.cuda.device(d):
+                    ranks.append(StepRequest(self._model(d), sh, y.to(torch.device("cuda", d)), dop=dop,
+                                             rank=r, num_steps=self.num_steps, guidance=self.guidance))
+            bufs = [r.exchange_buffers() for r in ranks]
+            for d in devs:
+                for e in devs:
+                    if d != e and torch.cuda.can_device_access_peer(d, e):
+                        check(lib().ddit_enable_peer_access(d, e))
+            for r in ranks:
+                r.set_peers([b[0] for b in bufs], [b[1] for b in bufs], [b[2] for b in bufs])
+            group = None
+        shards = []
+        for r, d in zip(ranks, devs):
+            Tl = r.shard.t_hi - r.shard.t_lo
+            shards.append(torch.empty((1, self.cfg.in_channels, Tl, *sh.latent[1:]),
+                                      device=torch.device("cuda", d)))
+        return _Live(tuple(gpu_ids), ranks, shards, group)
+
+    # ---------------------------------------------------------------- StepExecutor protocol
+    def dit_step(self, request: RequestState, gpu_ids: tuple[int, ...], step: int,
+                 resharded_from: tuple[int, ...] | None) -> float:
+        t0 = time.perf_counter()
+        live = self.live.get(request.request_id)
+        if live is None:  # first step: latent z0 sharded over the group
+            live = self._open(request, gpu_ids)
+            z0, _ = self._inputs(request)
+            for r, zs in zip(live.ranks, live.shards):
+                zs.copy_(z0[:, :, r.shard.t_lo:r.shard.t_hi])
+            self.live[request.request_id] = live
+        elif tuple(gpu_ids) != live.gpu_ids:  # promotion P -> P': re-shard at the boundary
+            new = self._open(request, gpu_ids)
+            srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
+            for r, zs in zip(new.ranks, new.shards):
+                with torch.cuda.device(zs.device):
+                    latent_gather(zs, r.shard.t_lo, r.shard.t_hi, srcs)
+            for d in {zs.device.index for zs in new.shards}:
+                torch.cuda.synchronize(d)
+            self.reshard_seconds.append(time.perf_counter() - t0)
+            new.steps_done = live.steps_done
+            new.history = live.history + [live.gpu_ids]
+            self._close(live)
+            self.live[request.request_id] = live = new
+        secs = self._run_step(live, step)
+        live.steps_done += 1
+        self.step_seconds.append((request.request_id, len(gpu_ids), secs))
+        if resharded_from is not None and self.reshard_seconds:
+            secs += self.reshard_seconds[-1]
+        return secs
+
+    def vae(self, request: RequestState, dit_gpu_ids: tuple[int, ...],
+            vae_gpu_ids: tuple[int, ...]) -> float:
+        """DiT -> VAE hand-off: the lowest-id retained GPU gathers the whole latent (K12)."""
+        live = self.live.pop(request.request_id)
+        sh = self._shape(request)
+        master = self.device_of(vae_gpu_ids[0])
+        t0 = time.perf_counter()
+        with torch.cuda.device(master):
+            z = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
+            srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
+            latent_gather(z, 0, sh.T, srcs)
+            torch.cuda.synchronize(master)
+        self.final_latents[request.request_id] = z
+        self._close(live)
+        return time.perf_counter() - t0
+
+    # ---------------------------------------------------------------- internals
+    def _run_step(self, live: _Live, step: int) -> float:
+        step = min(step, self.num_steps - 1)
+        if live.group is not None:
+            dev = live.shards[0].device
+            with torch.cuda.device(dev):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                live.group.step(live.shards, step)
+                e.record()
+                e.synchronize()
+                return s.elapsed_time(e) / 1e3
+        evs = []
+        for r, zs in zip(live.ranks, live.shards):
+            with torch.cuda.device(zs.device):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                r.step(zs, step)
+                e.record()
+                evs.append((s, e))
+        for _, e in evs:
+            e.synchronize()
+        return max(s.elapsed_time(e) for s, e in evs) / 1e3
+
+    def _close(self, live: _Live) -> None:
+        for r in live.ranks:
+            r.close()
+
+
+def profile_b200(cfg: STDiTConfig, weights: dict[str, torch.Tensor], labels: list[str],
+                 dops=(1, 2, 4, 8), repeats: int = 3, vae_seconds: dict[str, float] | None = None,
+                 gpu_ids_of=None) -> dict:
+    """Measure dit_step_seconds per (resolution, DoP) on this machine's GPUs and return a
+    ``dit-profile/1`` document (reference profiles.py:132-215). DoPs beyond the visible device
+    count run as virtual ranks on one device (flagged ``"virtual": true`` in the entry)."""
+    ex = B200Executor(cfg, weights)
+    entries = []
+    for res in labels:
+        for d in dops:
+            req = RequestState(10_000 + len(entries), res, 0.0, 30)
+            ids = tuple(range(d)) if gpu_ids_of is None else gpu_ids_of(d)
+            ex.dit_step(req, ids, 0, None)  # warm-up + open
+            times = [ex._run_step(ex.live[req.request_id], 1 + i) for i in range(repeats)]
+            ex._close(ex.live.pop(req.request_id))
+            e = {"resolution": res, "dop": d, "dit_step_seconds": min(times)}
+            if len({ex.device_of(g) for g in ids}) < d:
+                e["virtual"] = True
+            if d == 1:
+                e["vae_seconds"] = (vae_seconds or {}).get(res, 1e-6)
+            entries.append(e)
+    return {"schema": "dit-profile/1", "dop_candidates": list(dops), "entries": entries}

@@ -1,0 +1,87 @@
+"""The reference serving loop semantics driving real B200 steps: greedy allocator decisions with
+promotions (re-shard P -> P' at step boundaries) and the DiT -> VAE latent hand-off. The final
+latent of every request must equal running the same steps at DoP 1 (sharding, exchange and
+re-shards are numerically invisible)."""
+import dataclasses
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _profile_doc():
+    # synthetic times shaped so 144p-16f wants DoP 2 and 240p-like wants 4 (promotions happen)
+    return {"schema": "dit-profile/1", "dop_candidates": [1, 2, 4], "entries": [
+        {"resolution": "144p-16f", "dop": 1, "dit_step_seconds": 0.5, "vae_seconds": 0.2},
+        {"resolution": "144p-16f", "dop": 2, "dit_step_seconds": 0.25},
+        {"resolution": "144p-16f", "dop": 4, "dit_step_seconds": 0.24},
+        {"resolution": "144p", "dop": 1, "dit_step_seconds": 0.8, "vae_seconds": 0.3},
+        {"resolution": "144p", "dop": 2, "dit_step_seconds": 0.4},
+        {"resolution": "144p", "dop": 4, "dit_step_seconds": 0.15},
+    ]}
+
+
+def test_engine_drives_real_steps_with_promotions(cuda):
+    from paper_2506_13497_b200 import sched, shapes, weights
+    from paper_2506_13497_b200.executor import B200Executor
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W = weights.init_weights(cfg, seed=3)
+    steps = 8
+    ex = B200Executor(cfg, W, num_steps=steps)
+    t = sched.load_profiles(_profile_doc())
+    dt = sched.derive_dop_table(t)
+    assert dt.by_resolution == {"144p-16f": 2, "144p": 4}
+    # request 0 takes GPUs (0,1); request 1 starts hungry on (2,3) and is promoted to 4 GPUs
+    # once request 0's short DiT and VAE release (0,1)
+    wl = [sched.ArrivalRecord(0, 0.0, "144p-16f", 2), sched.ArrivalRecord(1, 0.0, "144p", steps),
+          sched.ArrivalRecord(2, 0.0, "144p-16f", 3), sched.ArrivalRecord(3, 0.0, "144p", 5)]
+    sim = sched.Simulation(sched.ClusterTopology(1, 4), t, dt, wl, sched.GreedyPolicy(dt), executor=ex)
+    res = sim.run()
+    kinds = [r.kind for r in res.trace]
+    assert kinds.count("vae_complete") == 4
+    assert "promotion" in kinds, "scenario must exercise a promotion"
+    assert len(ex.final_latents) == 4
+    # every request's final latent == the same steps at DoP 1
+    model = STDiTModel(cfg, W, cuda)
+    for rec in wl:
+        sh = shapes.shape_of(rec.resolution)
+        z, y = weights.synthetic_inputs(cfg, sh.latent, seed_z=2 * rec.request_id, seed_y=2 * rec.request_id + 1)
+        req = StepRequest(model, sh, y.to(cuda), num_steps=steps)
+        zd = z.to(cuda).contiguous()
+        for i in range(rec.denoise_steps):
+            req.step(zd, i)
+        torch.cuda.synchronize()
+        assert torch.equal(ex.final_latents[rec.request_id], zd), rec.request_id
+
+
+def test_latent_gather_regroups_shards(cuda):
+    from paper_2506_13497_b200.executor import latent_gather
+    from paper_2506_13497_b200 import shapes
+
+    T = 15
+    z = torch.randn(1, 4, T, 18, 32, device=cuda)
+    for P, Q in [(1, 2), (2, 4), (4, 8), (2, 1), (8, 1), (1, 8)]:
+        src = []
+        for r in range(P):
+            lo, hi = shapes.shard_range(T, P, r)
+            src.append((z[:, :, lo:hi].contiguous(), lo, hi))
+        for q in range(Q):
+            lo, hi = shapes.shard_range(T, Q, q)
+            d = torch.empty(1, 4, hi - lo, 18, 32, device=cuda)
+            latent_gather(d, lo, hi, src)
+            torch.cuda.synchronize()
+            assert torch.equal(d, z[:, :, lo:hi])
+
+
+def test_profile_b200_emits_loadable_document(cuda):
+    from paper_2506_13497_b200 import sched, weights
+    from paper_2506_13497_b200.executor import profile_b200
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W = weights.init_weights(cfg, seed=3)
+    doc = profile_b200(cfg, W, ["144p-16f"], dops=(1, 2), repeats=2, vae_seconds={"144p-16f": 0.1})
+    t = sched.load_profiles(doc)
+    assert t.dit_step("144p-16f", 1) > 0 and t.dit_step("144p-16f", 2) > 0
