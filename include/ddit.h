@@ -223,6 +223,49 @@ DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count);
 /* Total kernel launches issued by libddit in this process. */
 DDIT_API unsigned long long ddit_launch_count(void);
 
+/* ------------------------------------------------------------------ VAE decode kernels (K13)
+ * Implicit-GEMM convolution on tcgen05 over channels-last bf16 activations [B][T][H][W][C]
+ * (T = 1 for 2-D). Weights bf16 [Cout][kt][kh][kw][Cin]; "same" zero padding in H, W; in T
+ * either centred or causal (kt-1 frames of zeros in front, OpenSora CausalConv3d). Optional
+ * fp32 bias [Cout] and bf16 residual [B][T][H][W][Cout] added in the epilogue.
+ * Cin, Cout multiples of 64. */
+typedef struct ddit_conv_args {
+  const void* x;
+  void* y;
+  const void* w;
+  const float* bias;
+  const void* residual;
+  int B, T, H, W, Cin, Cout;
+  int kt, kh, kw;
+  int causal_time;
+} ddit_conv_args;
+DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream);
+
+/* GroupNorm over channels-last x [N][P][C] bf16 (per sample n, group of C/G channels, all P
+ * pixels), affine, optional SiLU -> y bf16. stats: device fp64 scratch [N][G][2]. */
+DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
+                            const float* beta, int N, int P, int C, int G, float eps, int silu_act,
+                            void* stream);
+/* nearest 2x in H and W: [N][H][W][C] -> [N][2H][2W][C] bf16 */
+DDIT_API int ddit_upsample2x(const void* x, void* y, int N, int H, int W, int C, void* stream);
+/* OpenSora temporal upsampling: [B][T][HW][2C] (channel 2c+ts) -> [B][2T][HW][C] bf16 */
+DDIT_API int ddit_depth_to_time(const void* x, void* y, int B, int T, int HW, int C, void* stream);
+/* Direct conv (CUDA cores) for layers with < 64 channels on one side. x strided
+ * (x_strides = element strides {b, c, t, h, w}, NULL = dense channels-last), bf16 or fp32;
+ * w fp32 [Cout][kt][kh][kw][Cin]; y bf16 channels-last, or fp32 [B][Cout][T][Hc][Wc] cropped
+ * when out_cf. */
+DDIT_API int ddit_conv_small(const void* x, int x_is_f32, const long long* x_strides,
+                             const float* w, const float* bias, void* y, int B, int T, int H, int W,
+                             int Cin, int Cout, int kt, int kh, int kw, int causal_time, int out_cf,
+                             int Hc, int Wc, void* stream);
+/* mid-block attention helpers: row softmax (fp32 S -> bf16 P, columns >= valid -> 0),
+ * bf16 transpose with zero-padded output rows, y = bf16(a_f32 + b_bf16) */
+DDIT_API int ddit_softmax_rows(const float* S, void* P, int rows, int cols, int valid, float scale,
+                               void* stream);
+DDIT_API int ddit_transpose_bf16(const void* in, void* out, int rows, int cols, int ld_in,
+                                 int rows_pad, void* stream);
+DDIT_API int ddit_add_f32_bf16(const float* a, const void* b, void* y, uint64_t n, void* stream);
+
 /* ------------------------------------------------------------------ re-sharding (K11 / K12)
  * dst (fp32 [channels][t_hi-t_lo][hw], this rank's new T-shard) <- frames gathered from up to
  * 16 source shards src[k] ([channels][src_t_hi[k]-src_t_lo[k]][hw], peer or local pointers).

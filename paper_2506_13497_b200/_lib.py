@@ -100,6 +100,14 @@ class CReqDesc(ctypes.Structure):
     ]
 
 
+class ConvArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", vp), ("y", vp), ("w", vp), ("bias", vp), ("residual", vp),
+        ("B", ci), ("T", ci), ("H", ci), ("W", ci), ("Cin", ci), ("Cout", ci),
+        ("kt", ci), ("kh", ci), ("kw", ci), ("causal_time", ci),
+    ]
+
+
 class Attn(ctypes.Structure):
     _fields_ = [
         ("q", ctypes.c_void_p), ("ldq", ctypes.c_int),
@@ -138,6 +146,14 @@ _SIGNATURES = {
     "ddit_request_profile": [vp, ci],
     "ddit_request_set_option": [vp, ci, ci],
     "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
+    "ddit_conv": [ctypes.POINTER(ConvArgs), vp],
+    "ddit_groupnorm": [vp, vp, vp, vp, vp, ci, ci, ci, ci, cf, ci, vp],
+    "ddit_upsample2x": [vp, vp, ci, ci, ci, ci, vp],
+    "ddit_depth_to_time": [vp, vp, ci, ci, ci, ci, vp],
+    "ddit_conv_small": [vp, ci, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, vp],
+    "ddit_softmax_rows": [vp, vp, ci, ci, ci, cf, vp],
+    "ddit_transpose_bf16": [vp, vp, ci, ci, ci, ci, vp],
+    "ddit_add_f32_bf16": [vp, vp, vp, ctypes.c_uint64, vp],
     "ddit_latent_gather": [vp, ci, ci, ctypes.POINTER(vp), ctypes.POINTER(ci), ctypes.POINTER(ci),
                            ci, ci, ci, vp],
     "ddit_ipc_export": [vp, vp, ctypes.POINTER(ctypes.c_uint64)],

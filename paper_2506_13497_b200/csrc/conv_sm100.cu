@@ -1,0 +1,405 @@
+// Implicit-GEMM convolution on tcgen05 for the VAE decoder.
+//
+// Activations are channels-last bf16 [B][T][H][W][C] (T = 1 for the 2-D spatial decoder).
+// One output tile = 128 pixels (R rows x Wt columns of one frame) x BN output channels.
+// The K loop runs over (tap, 64-channel block): for tap (dt, dy, dx) the producer TMA-loads
+// the input box {64 ch, Wt, R, 1, 1} at (c0, x0+dx-pw, y0+dy-ph, t+dt-pt, b) through a 5-D
+// tensor map -- coordinates outside the tensor are zero-filled, which IS the zero padding of
+// the convolution (spatial "same" padding and the causal front padding in time of
+// CausalConv3d). Weights are [Cout][taps][Cin] (K-major). Accumulation in TMEM (double
+// buffered), warp-specialised pipeline as in gemm_sm100.cu; the epilogue adds the bias and an
+// optional bf16 residual (TMA-loaded, prefetched one sub-tile ahead) and leaves through
+// swizzled smem + TMA stores clipped at the frame edges.
+#include "common.cuh"
+#include "ddit.h"
+#include "capi_internal.h"
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+namespace ddit {
+namespace conv {
+
+constexpr int BM = 128, BK = 64, THREADS = 256, TMEM_COLS = 512, ACC_STRIDE = 256;
+
+template <int BN, bool RES>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int EPI = 2 * 16384;  // staging (64 bf16 channels x 128 rows, SW128) x 2
+  static constexpr int BAR = 256;
+  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - EPI) / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR;
+};
+
+struct Params {
+  int B, T, H, W, Cin, Cout;
+  int kt, kh, kw, pt, ph, pw;
+  int Wt, R, x_tiles, y_tiles, n_tiles, num_tiles;
+  int cblocks, k_blocks;
+  int a_bytes;
+  const float* bias;
+};
+
+DDIT_DEV void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                          int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(c4)
+      : "memory");
+}
+DDIT_DEV void tma_store_5d(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3,
+                           int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+DDIT_DEV void ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DDIT_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
+DDIT_DEV void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+DDIT_DEV uint4 lds4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+
+struct TileCoord {
+  int b, t, y0, x0, n0;
+};
+DDIT_DEV TileCoord decode(const Params& p, int tile, int BN) {
+  TileCoord c;
+  const int nt = tile % p.n_tiles;
+  int pix = tile / p.n_tiles;
+  const int xt = pix % p.x_tiles;
+  pix /= p.x_tiles;
+  const int yt = pix % p.y_tiles;
+  pix /= p.y_tiles;
+  c.t = pix % p.T;
+  c.b = pix / p.T;
+  c.y0 = yt * p.R;
+  c.x0 = xt * p.Wt;
+  c.n0 = nt * BN;
+  return c;
+}
+
+template <int BN, bool RES>
+__global__ void __launch_bounds__(THREADS, 1)
+    conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                const __grid_constant__ Params p) {
+  using C = Cfg<BN, RES>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint8_t* sE = smem + STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + C::EPI);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  const int warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmY);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+      mbar_init(&rbar[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const TileCoord tc = decode(p, tile, BN);
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          const int tap = kb / p.cblocks, cb = kb % p.cblocks;
+          const int dx = tap % p.kw, dy = (tap / p.kw) % p.kh, dt = tap / (p.kw * p.kh);
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], p.a_bytes + C::B_BYTES);
+          tma_load_5d(sA + stage * C::A_BYTES, &tmX, &full[stage], cb * BK, tc.x0 + dx - p.pw,
+                      tc.y0 + dy - p.ph, tc.t + dt - p.pt, tc.b);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmW, &full[stage], kb * BK, tc.n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * ACC_STRIDE;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a = smem_u32(sA + stage * C::A_BYTES), b = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_ss(d, make_sdesc_sw128(a + 32 * k), make_sdesc_sw128(b + 32 * k), idesc,
+                         (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (kb == p.k_blocks - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int rit = ew * 32 + lane;
+    const bool elected = ew == 0 && lane == 0;
+    constexpr int NS = BN / 64;
+    int acc = 0, cnt = 0;
+    uint32_t acc_phase = 0;
+    if (RES && elected && (int)blockIdx.x < p.num_tiles) {
+      const TileCoord c0 = decode(p, blockIdx.x, BN);
+      mbar_arrive_expect_tx(&rbar[0], p.a_bytes);
+      tma_load_5d(sE, &tmR, &rbar[0], c0.n0, c0.x0, c0.y0, c0.t, c0.b);
+    }
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const TileCoord tc = decode(p, tile, BN);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * ACC_STRIDE;
+#pragma unroll 1
+      for (int sub = 0; sub < NS; ++sub) {
+        const int buf = cnt & 1;
+        uint8_t* sb = sE + buf * 16384;
+        const uint32_t sbase = smem_u32(sb);
+        if (elected) {
+          if (RES) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            const int nt = sub + 1 < NS ? tile : tile + (int)gridDim.x;
+            if (nt < p.num_tiles) {
+              const TileCoord c1 = sub + 1 < NS ? tc : decode(p, nt, BN);
+              const int nsub = sub + 1 < NS ? sub + 1 : 0;
+              mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
+              tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
+                          c1.y0, c1.t, c1.b);
+            }
+          } else {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (RES) mbar_wait(&rbar[buf], (cnt >> 1) & 1);
+        uint32_t r[64];
+        ld32(taddr + sub * 64, r);
+        ld32(taddr + sub * 64 + 32, r + 32);
+        tmem_ld_wait();
+        if (sub == NS - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int col0 = tc.n0 + sub * 64;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
+          if (p.bias) {
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j) + 1);
+            v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+            v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+          }
+          const uint32_t a = sbase + sw128(rit, j);
+          if (RES) {
+            const uint4 q = lds4(a);
+            const float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
+                         f3 = unpack_bf16(q.w);
+            v[0] += f0.x; v[1] += f0.y; v[2] += f1.x; v[3] += f1.y;
+            v[4] += f2.x; v[5] += f2.y; v[6] += f3.x; v[7] += f3.y;
+          }
+          sts4(a, pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+               pack_bf16(v[6], v[7]));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (elected) {
+          tma_store_5d(&tmY, sb, col0, tc.x0, tc.y0, tc.t, tc.b);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++cnt;
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encode encoder() {
+  static PFN_encode fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encode>(ptr);
+  });
+  return fn;
+}
+
+// channels-last [B][T][H][W][C] bf16, box {64, Wt, R, 1, 1}, 128 B swizzle
+static bool map_act(CUtensorMap* m, const void* base, int B, int T, int H, int W, int C, int Wt,
+                    int R) {
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T, (cuuint64_t)B};
+  cuuint64_t st[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2,
+                      (cuuint64_t)T * H * W * C * 2};
+  cuuint32_t box[5] = {64, (cuuint32_t)Wt, (cuuint32_t)R, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, st, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <int BN, bool RES>
+static int launch(const CUtensorMap& x, const CUtensorMap& w, const CUtensorMap& y,
+                  const CUtensorMap& r, const Params& p, int grid, cudaStream_t s) {
+  using C = Cfg<BN, RES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_kernel<BN, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  conv_kernel<BN, RES><<<grid, THREADS, C::SMEM, s>>>(x, w, y, r, p);
+  return check_cuda("conv_kernel");
+}
+
+}  // namespace conv
+}  // namespace ddit
+
+using namespace ddit;
+
+extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
+  using namespace conv;
+  if (!encoder()) {
+    set_error("conv: cuTensorMapEncodeTiled unavailable");
+    return DDIT_E_TMA;
+  }
+  if (a->Cin % 64 || a->Cout % 64 || a->B < 1 || a->T < 1 || a->H < 1 || a->W < 1) {
+    set_error("conv: Cin and Cout must be multiples of 64 (got %d, %d)", a->Cin, a->Cout);
+    return DDIT_E_INVALID;
+  }
+  const int bn = a->Cout % 256 == 0 ? 256 : (a->Cout % 128 == 0 ? 128 : 64);
+  Params p;
+  memset(&p, 0, sizeof p);
+  p.B = a->B; p.T = a->T; p.H = a->H; p.W = a->W; p.Cin = a->Cin; p.Cout = a->Cout;
+  p.kt = a->kt; p.kh = a->kh; p.kw = a->kw;
+  p.pt = a->causal_time ? a->kt - 1 : a->kt / 2;
+  p.ph = a->kh / 2;
+  p.pw = a->kw / 2;
+  p.Wt = a->W < 128 ? a->W : 128;
+  p.R = p.Wt == a->W ? 128 / a->W : 1;
+  if (p.R > a->H) p.R = a->H;
+  if (p.R < 1) p.R = 1;
+  p.x_tiles = (a->W + p.Wt - 1) / p.Wt;
+  p.y_tiles = (a->H + p.R - 1) / p.R;
+  p.n_tiles = a->Cout / bn;
+  p.num_tiles = a->B * a->T * p.y_tiles * p.x_tiles * p.n_tiles;
+  p.cblocks = a->Cin / 64;
+  p.k_blocks = a->kt * a->kh * a->kw * p.cblocks;
+  p.a_bytes = p.Wt * p.R * 128;
+  p.bias = a->bias;
+  CUtensorMap tx, tw, ty, tr;
+  memset(&tr, 0, sizeof tr);
+  bool ok = map_act(&tx, a->x, a->B, a->T, a->H, a->W, a->Cin, p.Wt, p.R) &&
+            map_act(&ty, a->y, a->B, a->T, a->H, a->W, a->Cout, p.Wt, p.R);
+  if (ok && a->residual) ok = map_act(&tr, a->residual, a->B, a->T, a->H, a->W, a->Cout, p.Wt, p.R);
+  {
+    const int K = p.k_blocks * 64;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)a->Cout};
+    cuuint64_t st[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)bn};
+    cuuint32_t es[2] = {1, 1};
+    ok = ok && encoder()(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w), dims, st,
+                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!ok) {
+    set_error("conv: tensor map encoding failed");
+    return DDIT_E_TMA;
+  }
+  if (!a->residual) tr = ty;
+  const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool res = a->residual != nullptr;
+  switch (bn) {
+    case 256: return res ? launch<256, true>(tx, tw, ty, tr, p, grid, s) : launch<256, false>(tx, tw, ty, tr, p, grid, s);
+    case 128: return res ? launch<128, true>(tx, tw, ty, tr, p, grid, s) : launch<128, false>(tx, tw, ty, tr, p, grid, s);
+    default: return res ? launch<64, true>(tx, tw, ty, tr, p, grid, s) : launch<64, false>(tx, tw, ty, tr, p, grid, s);
+  }
+}

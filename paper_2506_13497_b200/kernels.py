@@ -93,3 +93,20 @@ def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
           lib().ddit_attention_tc if tc else lib().ddit_attention)
     check(fn(ctypes.byref(a), stream_ptr(stream)))
     return o
+
+
+def conv(x: torch.Tensor, w: torch.Tensor, *, bias: torch.Tensor | None = None,
+         residual: torch.Tensor | None = None, causal_time: bool = True, out=None, stream=None):
+    """Implicit-GEMM conv on tcgen05. x: [B,T,H,W,Cin] bf16 (channels-last);
+    w: [Cout,kt,kh,kw,Cin] bf16; returns [B,T,H,W,Cout] bf16."""
+    from ._lib import ConvArgs
+
+    B, T, H, W, Cin = x.shape
+    Cout, kt, kh, kw, Cin2 = w.shape
+    assert Cin == Cin2 and x.is_contiguous() and w.is_contiguous()
+    if out is None:
+        out = torch.empty(B, T, H, W, Cout, dtype=torch.bfloat16, device=x.device)
+    a = ConvArgs(ptr(x), ptr(out), ptr(w), _c(bias), _c(residual), B, T, H, W, Cin, Cout, kt, kh,
+                 kw, 1 if causal_time else 0)
+    check(lib().ddit_conv(ctypes.byref(a), stream_ptr(stream)))
+    return out

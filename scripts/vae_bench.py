@@ -1,0 +1,30 @@
+"""Time the full OpenSora VAE decode of a 240p x 51 latent on one B200."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+from paper_2506_13497_b200 import shapes, vae_weights as vw
+from paper_2506_13497_b200.vae import VAEDecoder, vae_flops
+
+label = sys.argv[1] if len(sys.argv) > 1 else "240p"
+sh = shapes.shape_of(label)
+cfg = vw.OPENSORA_VAE
+dev = torch.device("cuda:0")
+dec = VAEDecoder(cfg, vw.init_vae_weights(cfg, device=dev), dev)
+z = torch.randn(1, 4, *sh.latent, device=dev)
+for _ in range(2):
+    out = dec.decode(z, sh.frames, sh.height, sh.width)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+n0 = dec.launches
+s.record()
+out = dec.decode(z, sh.frames, sh.height, sh.width)
+e.record()
+torch.cuda.synchronize()
+ms = s.elapsed_time(e)
+fl = vae_flops(cfg, sh.frames, sh.T, *sh.latent[1:])
+print(f"VAE decode {label}x{sh.frames}: {ms:.1f} ms, {fl / 1e12:.1f} TFLOP -> {fl / ms / 1e9:.0f} TFLOP/s, "
+      f"launches {dec.launches - n0}, out {tuple(out.shape)} finite={torch.isfinite(out).all().item()}")

@@ -1,0 +1,47 @@
+"""tcgen05 implicit-GEMM convolution vs torch fp32 conv (same op, same bf16-rounded inputs)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    return (torch.linalg.vector_norm(a.float() - b.float()) / torch.linalg.vector_norm(b.float())).item()
+
+
+def ref_conv(x, w, bias, residual, causal):
+    # x [B,T,H,W,C] -> torch NCTHW
+    xt = x.float().permute(0, 4, 1, 2, 3)
+    wt = w.float().permute(0, 4, 1, 2, 3)
+    kt, kh, kw = w.shape[1:4]
+    pt = (kt - 1, 0) if causal else (kt // 2, kt // 2)
+    xt = F.pad(xt, (kw // 2, kw // 2, kh // 2, kh // 2, *pt))
+    y = F.conv3d(xt, wt, bias.float() if bias is not None else None)
+    y = y.permute(0, 2, 3, 4, 1)
+    if residual is not None:
+        y = y + residual.float()
+    return y
+
+
+@pytest.mark.parametrize("B,T,H,W,Cin,Cout,k", [
+    (2, 1, 30, 54, 128, 256, (1, 3, 3)),     # 2-D, narrow frame (2 rows per tile)
+    (1, 1, 60, 107, 64, 128, (1, 3, 3)),     # odd width
+    (1, 1, 24, 300, 128, 64, (1, 3, 3)),     # wide frame (3 column tiles)
+    (1, 5, 12, 20, 128, 128, (3, 3, 3)),     # causal 3-D
+    (2, 3, 8, 16, 64, 256, (1, 1, 1)),       # 1x1 shortcut
+    (1, 4, 10, 10, 256, 512, (3, 3, 3)),
+])
+@pytest.mark.parametrize("with_res", [False, True])
+def test_conv_matches_torch(cuda, B, T, H, W, Cin, Cout, k, with_res):
+    from paper_2506_13497_b200 import kernels
+
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(B, T, H, W, Cin, generator=g).to(cuda, torch.bfloat16)
+    w = (torch.randn(Cout, *k, Cin, generator=g) / (Cin * k[0] * k[1] * k[2]) ** 0.5).to(cuda, torch.bfloat16)
+    bias = (0.1 * torch.randn(Cout, generator=g)).to(cuda)
+    res = torch.randn(B, T, H, W, Cout, generator=g).to(cuda, torch.bfloat16) if with_res else None
+    y = kernels.conv(x, w, bias=bias, residual=res, causal_time=True)
+    ref = ref_conv(x, w, bias, res, True)
+    torch.cuda.synchronize()
+    assert rel_l2(y, ref) < 1e-2
