@@ -242,7 +242,8 @@ typedef struct ddit_conv_args {
 DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream);
 
 /* GroupNorm over channels-last x [N][P][C] bf16 (per sample n, group of C/G channels, all P
- * pixels), affine, optional SiLU -> y bf16. stats: device fp64 scratch [N][G][2]. */
+ * pixels), affine, optional SiLU -> y bf16. Deterministic (fixed reduction order).
+ * stats: device scratch of at least N*G*2 doubles + N*512*G float2. */
 DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
                             const float* beta, int N, int P, int C, int G, float eps, int silu_act,
                             void* stream);

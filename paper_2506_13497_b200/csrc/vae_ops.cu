@@ -1,6 +1,6 @@
 // Memory-bound and small-channel kernels of the VAE decoder, all on
 // channels-last activations [N][P][C] (N samples, P = T*H*W pixels):
-//   GroupNorm statistics (fp64 accumulation of per-block fp32 partials) + normalise / affine /
+//   GroupNorm statistics (deterministic: per-block fp32 partials, fixed-order fp64 sum) + normalise / affine /
 //   optional SiLU; nearest 2x spatial upsample; depth-to-time (OpenSora temporal upsampler
 //   "B (C ts) T H W -> B C (T ts) H W"); direct convolutions for the few layers with fewer than
 //   64 channels on one side (latent in, frames out); row softmax and transpose for the
@@ -12,22 +12,21 @@
 namespace ddit {
 
 // ------------------------------------------------------------------ GroupNorm
-// x: [N][P][C] bf16; stats: fp64 [N][G][2] (sum, sumsq), zero-initialised by the caller.
-// Thread t owns the fixed 8-channel vector t % (C/8) (C/8 divides 256) and walks pixels with
-// stride 256 / (C/8); per-thread fp32 partials -> smem group bins -> fp64 global atomics.
+// Deterministic two-level statistics (fixed reduction order: bitwise reproducible).
+// gn_partial: block (blk, n) reduces pixels [blk*ppb, (blk+1)*ppb) of sample n into
+// partial[n][blk][g] = (sum, sumsq); thread t owns the 8-channel vector t % (C/8) (C/8 divides
+// 256) and walks pixels with stride 256 / (C/8).
 __global__ void __launch_bounds__(256)
-    gn_stats_kernel(const __nv_bfloat16* __restrict__ x, double* __restrict__ stats, int P, int C,
-                    int G, int pix_per_block) {
-  const int n = blockIdx.y;
+    gn_partial_kernel(const __nv_bfloat16* __restrict__ x, float2* __restrict__ partial, int P,
+                      int C, int G, int ppb, int nblk) {
+  const int n = blockIdx.y, blk = blockIdx.x;
   const int cg = C / G;
   const int vecs = C / 8;
   const int step = 256 / vecs;
   const int v = threadIdx.x % vecs;
-  const int p0 = blockIdx.x * pix_per_block;
-  const int p1 = min(p0 + pix_per_block, P);
-  __shared__ float bin_s[32], bin_q[32];
-  if (threadIdx.x < 32) bin_s[threadIdx.x] = bin_q[threadIdx.x] = 0.f;
-  __syncthreads();
+  const int p0 = blk * ppb;
+  const int p1 = min(p0 + ppb, P);
+  __shared__ float red_s[256][9], red_q[256][9];
   float sg[8], qg[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) sg[e] = qg[e] = 0.f;
@@ -45,15 +44,38 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const int g = (v * 8 + e) / cg;
-    atomicAdd(&bin_s[g], sg[e]);
-    atomicAdd(&bin_q[g], qg[e]);
+    red_s[threadIdx.x][e] = sg[e];
+    red_q[threadIdx.x][e] = qg[e];
   }
   __syncthreads();
   if (threadIdx.x < G) {
-    atomicAdd(&stats[(n * G + threadIdx.x) * 2], (double)bin_s[threadIdx.x]);
-    atomicAdd(&stats[(n * G + threadIdx.x) * 2 + 1], (double)bin_q[threadIdx.x]);
+    const int g = threadIdx.x;
+    float s = 0.f, q = 0.f;
+    for (int t = 0; t < 256; ++t) {
+      const int c0 = (t % vecs) * 8;
+      if (c0 + 8 <= g * cg || c0 >= (g + 1) * cg) continue;
+      for (int e = 0; e < 8; ++e)
+        if ((c0 + e) / cg == g) {
+          s += red_s[t][e];
+          q += red_q[t][e];
+        }
+    }
+    partial[((size_t)n * nblk + blk) * G + g] = make_float2(s, q);
   }
+}
+
+__global__ void gn_finalize_kernel(const float2* __restrict__ partial, double* __restrict__ stats,
+                                   int G, int nblk) {
+  const int n = blockIdx.x, g = threadIdx.x;
+  if (g >= G) return;
+  double s = 0, q = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const float2 v = partial[((size_t)n * nblk + b) * G + g];
+    s += v.x;
+    q += v.y;
+  }
+  stats[(n * G + g) * 2] = s;
+  stats[(n * G + g) * 2 + 1] = q;
 }
 
 // y = act((x - mean) * rstd * gamma + beta), act = SiLU or identity; bf16 in / out.
@@ -257,15 +279,22 @@ extern "C" {
 DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
                             const float* beta, int N, int P, int C, int G, float eps, int silu_act,
                             void* stream) {
+  // `stats` scratch layout: fp64 [N][G][2] followed by the fp32x2 partials [N][nblk][G]
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (C % 8 || C % G || G > 32 || (C / 8) > 256 || 256 % (C / 8)) {
     set_error("groupnorm: C a power of two in [8, 2048] divisible by G <= 32 required");
     return DDIT_E_INVALID;
   }
-  cudaMemsetAsync(stats, 0, sizeof(double) * N * G * 2, s);
-  const int ppb = 1024;
-  dim3 grid((P + ppb - 1) / ppb, N);
-  gn_stats_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), stats, P, C, G, ppb);
+  int ppb = 1024;
+  int nblk = (P + ppb - 1) / ppb;
+  if (nblk > 512) {  // bound the partial buffer: larger pixel chunks per block
+    ppb = (P + 511) / 512;
+    nblk = (P + ppb - 1) / ppb;
+  }
+  float2* partial = reinterpret_cast<float2*>(stats + (size_t)N * G * 2);
+  gn_partial_kernel<<<dim3(nblk, N), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), partial, P,
+                                                  C, G, ppb, nblk);
+  gn_finalize_kernel<<<N, 32, 0, s>>>(partial, stats, G, nblk);
   const size_t vecs = (size_t)N * P * (C / 8);
   gn_apply_kernel<<<blocks_for(vecs, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
                                                          static_cast<__nv_bfloat16*>(y), stats,

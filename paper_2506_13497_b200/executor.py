@@ -66,7 +66,8 @@ class B200Executor:
 
     def __init__(self, cfg: STDiTConfig, weights: dict[str, torch.Tensor], *,
                  shapes: dict[str, VideoShape] | None = None, num_steps: int = 30,
-                 guidance: float = 7.0, seed_base: int = 0):
+                 guidance: float = 7.0, seed_base: int = 0, vae_cfg=None, vae_weights=None,
+                 keep_videos: bool = False):
         self.cfg = cfg
         self.ndev = max(torch.cuda.device_count(), 1)
         self.models: dict[int, STDiTModel] = {}
@@ -79,6 +80,12 @@ class B200Executor:
         self.final_latents: dict[int, torch.Tensor] = {}
         self.step_seconds: list[tuple[int, int, float]] = []  # (request, dop, seconds)
         self.reshard_seconds: list[float] = []
+        self.vae_cfg = vae_cfg
+        self._vae_weights = vae_weights
+        self.vaes: dict[int, object] = {}
+        self.keep_videos = keep_videos
+        self.videos: dict[int, torch.Tensor] = {}
+        self.vae_seconds: list[tuple[int, float, float]] = []  # (request, handoff s, decode s)
 
     # ---------------------------------------------------------------- helpers
     def device_of(self, gpu_id: int) -> int:
@@ -162,9 +169,17 @@ class B200Executor:
             secs += self.reshard_seconds[-1]
         return secs
 
+    def _vae(self, dev: int):
+        if dev not in self.vaes:
+            from .vae import VAEDecoder
+
+            self.vaes[dev] = VAEDecoder(self.vae_cfg, self._vae_weights, torch.device("cuda", dev))
+        return self.vaes[dev]
+
     def vae(self, request: RequestState, dit_gpu_ids: tuple[int, ...],
             vae_gpu_ids: tuple[int, ...]) -> float:
-        """DiT -> VAE hand-off: the lowest-id retained GPU gathers the whole latent (K12)."""
+        """DiT -> VAE hand-off: the lowest-id retained GPU gathers the whole latent (K12), then
+        (when a VAE is configured) decodes it to frames on that GPU (K13)."""
         live = self.live.pop(request.request_id)
         sh = self._shape(request)
         master = self.device_of(vae_gpu_ids[0])
@@ -174,9 +189,22 @@ class B200Executor:
             srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
             latent_gather(z, 0, sh.T, srcs)
             torch.cuda.synchronize(master)
+        handoff = time.perf_counter() - t0
         self.final_latents[request.request_id] = z
         self._close(live)
-        return time.perf_counter() - t0
+        decode = 0.0
+        if self.vae_cfg is not None:
+            with torch.cuda.device(master):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                video = self._vae(master).decode(z, sh.frames, sh.height, sh.width)
+                e.record()
+                e.synchronize()
+                decode = s.elapsed_time(e) / 1e3
+            if self.keep_videos:
+                self.videos[request.request_id] = video
+        self.vae_seconds.append((request.request_id, handoff, decode))
+        return handoff + decode
 
     # ---------------------------------------------------------------- internals
     def _run_step(self, live: _Live, step: int) -> float:
@@ -209,7 +237,7 @@ class B200Executor:
 
 def profile_b200(cfg: STDiTConfig, weights: dict[str, torch.Tensor], labels: list[str],
                  dops=(1, 2, 4, 8), repeats: int = 3, vae_seconds: dict[str, float] | None = None,
-                 gpu_ids_of=None) -> dict:
+                 gpu_ids_of=None, vae_cfg=None, vae_weights=None) -> dict:
     """Measure dit_step_seconds per (resolution, DoP) on this machine's GPUs and return a
     ``dit-profile/1`` document (reference profiles.py:132-215). DoPs beyond the visible device
     count run as virtual ranks on one device (flagged ``"virtual": true`` in the entry)."""
@@ -226,6 +254,20 @@ def profile_b200(cfg: STDiTConfig, weights: dict[str, torch.Tensor], labels: lis
             if len({ex.device_of(g) for g in ids}) < d:
                 e["virtual"] = True
             if d == 1:
-                e["vae_seconds"] = (vae_seconds or {}).get(res, 1e-6)
+                if vae_cfg is not None:  # measured decode on one GPU (the VAE DoP DDiT uses)
+                    from .vae import VAEDecoder
+
+                    sh = shape_of(res)
+                    dec = VAEDecoder(vae_cfg, vae_weights, torch.device("cuda", 0))
+                    z = torch.randn((1, cfg.in_channels, *sh.latent), device="cuda:0")
+                    dec.decode(z, sh.frames, sh.height, sh.width)
+                    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s0.record()
+                    dec.decode(z, sh.frames, sh.height, sh.width)
+                    s1.record()
+                    s1.synchronize()
+                    e["vae_seconds"] = s0.elapsed_time(s1) / 1e3
+                else:
+                    e["vae_seconds"] = (vae_seconds or {}).get(res, 1e-6)
             entries.append(e)
     return {"schema": "dit-profile/1", "dop_candidates": list(dops), "entries": entries}

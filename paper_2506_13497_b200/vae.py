@@ -68,7 +68,8 @@ class VAEDecoder:
         self.w_qkv = _bf16(torch.cat([W[a + "to_q.weight"], W[a + "to_k.weight"], W[a + "to_v.weight"]]))
         self.b_qkv = torch.cat([W[a + "to_q.bias"], W[a + "to_k.bias"], W[a + "to_v.bias"]]).contiguous()
         self.w_out = _bf16(W[a + "to_out.weight"])
-        self.stats = torch.empty(4096 * 2, dtype=torch.float64, device=d)
+        # GroupNorm scratch: fp64 [N][G][2] + fp32x2 partials [N][512][G], N <= 256 samples
+        self.stats = torch.empty(256 * 32 * 2 + 256 * 512 * 32, dtype=torch.float64, device=d)
         self.launches = 0
 
     # ---------------------------------------------------------------- primitives

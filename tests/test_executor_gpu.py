@@ -85,3 +85,28 @@ def test_profile_b200_emits_loadable_document(cuda):
     doc = profile_b200(cfg, W, ["144p-16f"], dops=(1, 2), repeats=2, vae_seconds={"144p-16f": 0.1})
     t = sched.load_profiles(doc)
     assert t.dit_step("144p-16f", 1) > 0 and t.dit_step("144p-16f", 2) > 0
+
+
+def test_engine_with_vae_decode(cuda):
+    """Decoupled DiT -> VAE through the engine: the retained master GPU decodes the gathered
+    latent; the video equals decoding the DoP-1 latent."""
+    from paper_2506_13497_b200 import sched, shapes, weights, vae_weights as vw
+    from paper_2506_13497_b200.executor import B200Executor
+    from paper_2506_13497_b200.vae import VAEDecoder
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W = weights.init_weights(cfg, seed=3)
+    VW = vw.init_vae_weights(vw.TINY_VAE)
+    ex = B200Executor(cfg, W, num_steps=3, vae_cfg=vw.TINY_VAE, vae_weights=VW, keep_videos=True)
+    t = sched.load_profiles(_profile_doc())
+    dt = sched.derive_dop_table(t)
+    wl = [sched.ArrivalRecord(0, 0.0, "144p-16f", 3)]
+    res = sched.Simulation(sched.ClusterTopology(1, 4), t, dt, wl, sched.GreedyPolicy(dt), executor=ex).run()
+    assert [r.kind for r in res.trace][-1] == "vae_complete"
+    sh = shapes.shape_of("144p-16f")
+    video = ex.videos[0]
+    assert video.shape == (1, 3, sh.frames, sh.height, sh.width)
+    ref = VAEDecoder(vw.TINY_VAE, VW, cuda).decode(ex.final_latents[0], sh.frames, sh.height, sh.width)
+    torch.cuda.synchronize()
+    assert torch.equal(video, ref)
+    assert ex.vae_seconds[0][2] > 0
