@@ -41,6 +41,8 @@ DDIT_API int ddit_num_sms(void);
 /* GEMM kernel selection for plans built afterwards: 1 (default) = cta_group::2 kernel
  * (256-row tiles over a CTA pair), 0 = single-CTA kernel (128-row tiles). Env DDIT_GEMM_2CTA=0. */
 DDIT_API int ddit_set_gemm_2cta(int on);
+/* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
+DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */
 DDIT_API int ddit_enable_peer_access(int device, int peer);
 

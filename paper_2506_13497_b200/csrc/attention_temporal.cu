@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(TA_THREADS)
   extern __shared__ __align__(16) uint8_t ta_smem[];
   const int pitch = 3 * p.C + 8;  // +16 B: conflict-free ldmatrix rows
   __nv_bfloat16* sm = reinterpret_cast<__nv_bfloat16*>(ta_smem);
+  pdl_wait();
   const int pos = blockIdx.x;
   const int base_row = (pos / p.inner) * p.outer + (pos % p.inner);
   const int rows = NT * 8;
@@ -233,7 +234,7 @@ int temporal_attention_launch(const ddit_attn* a, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr[NT == 4] = true;
   }
-  kern<<<a->num_seqs, TA_THREADS, smem, s>>>(p);
+  launch_pdl(kern, dim3(a->num_seqs), dim3(TA_THREADS), smem, s, p);
   return check_cuda("temporal_attn_kernel");
 }
 

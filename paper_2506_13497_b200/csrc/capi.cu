@@ -72,6 +72,10 @@ DDIT_API int ddit_enable_peer_access(int device, int peer) {
   }
   return DDIT_OK;
 }
+DDIT_API int ddit_set_pdl(int on) {
+  set_pdl(on);
+  return DDIT_OK;
+}
 DDIT_API int ddit_set_gemm_2cta(int on) {
   set_two_cta(on);
   return DDIT_OK;

@@ -183,11 +183,35 @@ DDIT_DEV float2 unpack_bf16(uint32_t u) {
   return __bfloat1622float2(v);
 }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute waits here for its
+// predecessor grid (complete + memory visible) before touching global memory, after doing its
+// independent prologue; a primary signals that dependents may be scheduled.
+DDIT_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DDIT_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename T>
 DDIT_DEV T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Host: launch with the programmatic-stream-serialisation attribute (kernel must pdl_wait()).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace ddit

@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(256)
     ln_modulate_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int M, int C,
                        const float* __restrict__ shift, const float* __restrict__ scale,
                        int mod_stride, int rows_per_b, float eps) {
+  pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -63,8 +64,8 @@ __global__ void __launch_bounds__(256)
 int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
                 const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s) {
   if (C % 4 || C > 32 * 4 * kMaxVec || M <= 0) return -2;
-  ln_modulate_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, out, M, C, shift, scale, mod_stride,
-                                                  rows_per_b > 0 ? rows_per_b : M, eps);
+  launch_pdl(ln_modulate_kernel, dim3((M + 7) / 8), dim3(256), 0, s, x, out, M, C, shift, scale,
+             mod_stride, rows_per_b > 0 ? rows_per_b : M, eps);
   return 0;
 }
 

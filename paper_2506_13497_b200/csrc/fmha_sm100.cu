@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
 
   // work item -> (q tile, head, sequence); q tile fastest so concurrent CTAs share K/V in L2
   auto decode = [&](int wi, int& qt, int& head, int& seq) {
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
         }
       }
+      pdl_trigger();
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
     constexpr uint32_t id_qk = idesc_f16(128, 128, false);
@@ -598,8 +600,8 @@ int fmha_plan_launch(const FmhaPlan* fp, cudaStream_t s) {
     cudaFuncSetAttribute(fmha_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
     attr = true;
   }
-  fmha_sm100_kernel<<<fp->grid, fm::THREADS, fm::SMEM, s>>>(fp->tmQa, fp->tmQb, fp->tmKVa,
-                                                             fp->tmKVb, fp->tmO, fp->p);
+  launch_pdl(fmha_sm100_kernel, fp->grid, dim3(fm::THREADS), fm::SMEM, s, fp->tmQa, fp->tmQb,
+             fp->tmKVa, fp->tmKVb, fp->tmO, fp->p);
   return check_cuda("fmha_sm100_kernel");
 }
 

@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      pdl_trigger();  // all loads issued: dependents may start their prologue
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
@@ -638,6 +640,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0) {
     if (elect_one()) {  // ---- producer (both CTAs): own halves of A and B -> leader's barrier
@@ -660,6 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      pdl_trigger();
     }
   } else if (warp == 1) {
     if (rank == 0) {  // ---- MMA issuer (leader CTA only)
@@ -880,6 +884,16 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
   return 0;
 }
 
+static int g_pdl = -1;
+bool pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = getenv("DDIT_PDL");
+    g_pdl = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_pdl != 0;
+}
+void set_pdl(int on) { g_pdl = on ? 1 : 0; }
+
 static int g_two_cta = -1;
 bool two_cta_enabled() {
   if (g_two_cta < 0) {
@@ -903,8 +917,8 @@ static int launch_t2(const GemmPlan* p, cudaStream_t s) {
     }
     attr_set = true;
   }
-  gemm2_bf16_tn_kernel<BN, EPI><<<p->grid, kThreads, smem, s>>>(p->tmA, p->tmB, p->tmO, p->tmR,
-                                                                 p->tmO2, p->M, p->N, p->K, p->ep);
+  launch_pdl(gemm2_bf16_tn_kernel<BN, EPI>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
+             p->tmO, p->tmR, p->tmO2, p->M, p->N, p->K, p->ep);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "gemm2 launch: %s", cudaGetErrorString(e));
@@ -927,8 +941,8 @@ static int launch_t(const GemmPlan* p, cudaStream_t s) {
     }
     attr_set = true;
   }
-  gemm_bf16_tn_kernel<BN, EPI><<<p->grid, kThreads, smem, s>>>(p->tmA, p->tmB, p->tmO, p->tmR,
-                                                                p->tmO2, p->M, p->N, p->K, p->ep);
+  launch_pdl(gemm_bf16_tn_kernel<BN, EPI>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
+             p->tmO, p->tmR, p->tmO2, p->M, p->N, p->K, p->ep);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     snprintf(g_err, sizeof g_err, "gemm launch: %s", cudaGetErrorString(e));

@@ -59,6 +59,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
 int num_sms();
 bool two_cta_enabled();
+void set_pdl(int on);
 void set_two_cta(int on);
 const char* gemm_last_error();
 
