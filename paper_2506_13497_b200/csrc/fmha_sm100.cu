@@ -41,7 +41,7 @@ constexpr int OFF_V = OFF_K + KST * (KA + KB);       // VST V stages
 constexpr int OFF_P = OFF_V + VST * (VA + VB);       // 2 P buffers
 constexpr int OFF_OST = OFF_P + 2 * PBUF;            // O staging (128 x 144 B)
 constexpr int OFF_BAR = OFF_OST + 128 * 144;
-constexpr int SMEM = 1024 + OFF_BAR + 26 * 8 + 1024;
+constexpr int SMEM = 1024 + OFF_BAR + 26 * 8 + 3072;
 constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
 constexpr float RESCALE_LOG2 = 8.0f;
 }  // namespace fm
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   uint64_t* o_full = bars + 20;   // [2]
   uint64_t* o_free = bars + 22;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-  float* xmax = reinterpret_cast<float*>(bars + 26);  // [2][128] partial row maxima / sums
+  float* xmax = reinterpret_cast<float*>(bars + 26);  // [2 tile parity][2][128] partial row maxima, [2][128] row sums
 
   const int warp = warp_id(), lane = lane_id();
   const int nk = (p.Lk + BKV - 1) / BKV;
@@ -372,10 +372,12 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         }
         float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        xmax[half * 128 + row] = mx;
+        // tile-parity slots: the partner's read of slot t&1 precedes its arrival at tile t+1's
+        // barrier, so slot t&1 is free again at tile t+2 -- one barrier per tile
+        float* xm = xmax + (t & 1) * 256;
+        xm[half * 128 + row] = mx;
         asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        mx = fmaxf(mx, xmax[(half ^ 1) * 128 + row]);
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
         const float m_new = fmaxf(m, mx * p.scale_log2);
         const bool resc = m_new > m + RESCALE_LOG2;
         float alpha = 1.f;
@@ -470,10 +472,10 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[ob]);
-      xmax[half * 128 + row] = l;
+      xmax[512 + half * 128 + row] = l;
       if (elected) bulk_wait_read0();  // previous item's store no longer reads the staging
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      const float lt = l + xmax[(half ^ 1) * 128 + row];
+      const float lt = l + xmax[512 + (half ^ 1) * 128 + row];
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
       const uint32_t obase = smem_u32(sm + OFF_OST) + row * 144;
       const int c0 = half ? 5 : 0, nc = half ? 4 : 5;

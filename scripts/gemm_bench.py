@@ -39,3 +39,31 @@ for name, N, K, bn, epi in shapes:
     tc = s.elapsed_time(e) / it
     fl = 2 * m * N * K
     print(f"{name:8s} M={m} N={N} K={K} bn={bn}: ours {t*1e3:8.1f} us {fl/t/1e9:7.1f} TF/s | cublas {tc*1e3:8.1f} us {fl/tc/1e9:7.1f} TF/s", flush=True)
+
+# fp32 residual epilogue (proj / cproj / fc2): resid[m, n] += gate[b, n] * (a @ w.T + bias), with
+# and without the bf16 copy; reported against HBM bytes as well as FLOPs
+for name, N, K, bn, copy in [("proj_resid", 1152, 1152, 192, True), ("cproj_resid", 1152, 1152, 192, False),
+                             ("fc2_resid", 1152, 4608, 192, False), ("proj_r128", 1152, 1152, 128, True)]:
+    m = M
+    a = torch.randn(m, K, device=dev).bfloat16()
+    w = (torch.randn(N, K, device=dev) / math.sqrt(K)).bfloat16()
+    bias = torch.zeros(N, device=dev)
+    x = torch.randn(m, N, device=dev)
+    gate = torch.randn(2, N, device=dev)
+    o2 = torch.empty(m, N, device=dev, dtype=torch.bfloat16) if copy else None
+    f = lambda: kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=m // 2,
+                             out2=o2, bn=bn)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    it = 20
+    s.record()
+    for _ in range(it):
+        f()
+    e.record(); torch.cuda.synchronize()
+    t = s.elapsed_time(e) / it
+    fl = 2 * m * N * K
+    byt = m * K * 2 + N * K * 2 + m * N * 8 + (m * N * 2 if copy else 0)
+    print(f"{name:11s} M={m} N={N} K={K} bn={bn}: {t*1e3:8.1f} us {fl/t/1e9:7.1f} TF/s "
+          f"{byt/t/1e6:7.1f} GB/s (compulsory {byt/1e6:.0f} MB)", flush=True)
