@@ -48,7 +48,8 @@ def _digest(paths: list[Path]) -> str:
         if p.is_file():
             h.update(p.name.encode())
             h.update(p.read_bytes())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    # flags without the absolute include paths, so the stamp survives the move to the GPU box
+    h.update(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")]).encode())
     return h.hexdigest()[:16]
 
 

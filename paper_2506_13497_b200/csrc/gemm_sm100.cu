@@ -35,16 +35,24 @@ struct EpiCfg {
   static constexpr bool BF = EPI == EPI_BF16 || EPI == EPI_GELU_BF16;
   static constexpr int SUB = EPI == EPI_QKV ? 72 : BF ? (BN % 64 == 0 ? 64 : 32) : 32;
   static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
-  static constexpr int BUF2 = EPI == EPI_RESID ? 128 * 64 : 0;         // bf16 copy (SW64)
-  static constexpr int BYTES = 2 * (BUF + BUF2);
+  // gated residual: each epilogue warp runs its own ring of RSLOTS fp32 32x32 sub-tiles (loads run
+  // RSLOTS-2 sub-tiles ahead) + three bf16 copy buffers (SW64): WARP_BYTES per warp
+  static constexpr int RSLOTS = EPI == EPI_RESID ? 2 : 0;
+  // R >= 3: stores of sub-tile s-1 may still read while s runs (3 bf16 buffers, loads R-2 ahead);
+  // R == 2: they must finish first (2 bf16 buffers, loads 1 ahead)
+  static constexpr int RAHEAD = RSLOTS >= 3 ? RSLOTS - 2 : 1;
+  static constexpr int NOB = RSLOTS >= 3 ? 3 : 2;
+  static constexpr int WARP_BYTES = RSLOTS * 4096 + NOB * 2048;
+  static constexpr int BYTES = EPI == EPI_RESID ? 4 * WARP_BYTES : 2 * BUF;
 };
+static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
 
 template <int BN, int EPI>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int BUDGET = 232448 - 1024 - BAR_BYTES - EpiCfg<BN, EPI>::BYTES;
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -121,8 +129,45 @@ DDIT_DEV float gelu_fast(float x) {
 struct EpiCtx {
   int m_tiles, n_tiles, num_tiles;
   int M;
-  int next_m0, next_n0;  // this CTA's next tile (residual prefetch), next_m0 < 0: none
 };
+
+// The sequence of 128x32 residual sub-tiles this CTA's epilogue consumes: sub-tile j belongs to
+// the CTA's (j / NS)-th tile (tile0 + i * tstride) at column block j % NS.
+struct ResidStream {
+  int tile0, tstride, num_tiles, n_tiles, mstep, moff;
+  DDIT_DEV bool coord(int j, int ns, int& m0, int& c0) const {
+    const int t = tile0 + (j / ns) * tstride;
+    if (t >= num_tiles) return false;
+    m0 = (t / n_tiles) * mstep + moff;
+    c0 = (t % n_tiles) * (ns * 32) + (j % ns) * 32;
+    return true;
+  }
+};
+
+// Pull the i-th residual tile (this CTA's 128 rows x BN) of the stream into L2 ahead of its
+// epilogue; tmP is a box-{BN, 128} map of the residual (no swizzle, L2 prefetch only).
+template <int BN>
+DDIT_DEV void resid_prefetch_l2(const ResidStream& rs, int i, const CUtensorMap* tmP) {
+  int m0, c0;
+  if (rs.coord(i * (BN / 32), BN / 32, m0, c0))
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmP)),
+                 "r"(c0), "r"(m0)
+                 : "memory");
+}
+
+// load residual sub-tile j of this warp's 32-row slab into ring slot j % R (wbase: the warp's
+// ring, wbar: its R barriers)
+template <int R>
+DDIT_DEV void resid_issue(const ResidStream& rs, int ns, int j, int row_off, const CUtensorMap* tmR,
+                          uint8_t* wbase, uint64_t* wbar) {
+  int m0, c0;
+  if (rs.coord(j, ns, m0, c0)) {
+    const int slot = j % R;
+    mbar_arrive_expect_tx(&wbar[slot], 4096);
+    tma_load_2d(wbase + slot * 4096, tmR, &wbar[slot], c0, m0 + row_off);
+  }
+}
 
 DDIT_DEV void mbar_arrive_cl(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
@@ -210,47 +255,47 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
 // ------------------------------------------------------------------ epilogue: gated residual
 // x[r, c] += gate[b(r), c] * (acc + bias[c]) in fp32 through TMA (load, update in smem, store),
 // plus an optional bf16 copy of the new x (the cross-attention query input).
-// Coordinates of the residual sub-tile after (this tile, sub): the next sub-tile of the same
-// tile, else sub-tile 0 of this CTA's next tile (m_next < 0: none).
-struct ResidNext {
-  int m0, n0, sub;
-  bool valid;
-};
-
+// Every epilogue warp owns the 32 accumulator rows of its TMEM lane quarter and runs an
+// independent pipeline over them: its residual 32x32 sub-tiles stream through a private
+// RSLOTS-deep ring whose loads run RSLOTS-2 sub-tiles ahead (across tile boundaries), its own
+// TMA stores leave from the same slot, and no CTA-wide barrier is involved -- the four warps
+// drift freely, so one warp's HBM latency hides behind the others' math.
 template <int BN>
 DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const CUtensorMap* tmO2,
-                             uint8_t* sE, uint64_t* rbar, uint32_t taddr, int rit,
-                             int m0, int n0, const EpiCtx& cx, bool elected, int& cnt,
-                             uint32_t tempty_cl, int lane) {
+                             uint8_t* sE, uint64_t* rbar, uint32_t taddr, int ew, int lane,
+                             int m0, int n0, const EpiCtx& cx, const ResidStream& rs,
+                             int& cnt, uint32_t tempty_cl) {
   constexpr int NS = BN / 32;
-  const int row = m0 + rit;
+  constexpr int R = EpiCfg<BN, EPI_RESID>::RSLOTS;
+  uint8_t* wbase = sE + ew * EpiCfg<BN, EPI_RESID>::WARP_BYTES;
+  uint64_t* wbar = rbar + ew * R;
+  const int rit = lane;  // row within the warp's slab (swizzle phase = lane & 7)
+  const int row = m0 + ew * 32 + lane;
   const int grow = row < cx.M ? row : cx.M - 1;
   const float* gate_row = ep.gate ? ep.gate + (size_t)(grow / ep.rows_per_b) * ep.gate_stride : nullptr;
 #pragma unroll 1
   for (int sub = 0; sub < NS; ++sub) {
-    const int buf = cnt & 1;
-    uint8_t* rb = sE + buf * 16384;
-    uint8_t* ob = sE + 2 * 16384 + buf * 8192;
-    if (elected) {
-      bulk_wait_read<0>();  // buffer buf^1 (previous sub-tile) no longer read by its stores
-      ResidNext nx;
-      if (sub + 1 < NS) {
-        nx.valid = true;
-        nx.m0 = m0;
-        nx.n0 = n0;
-        nx.sub = sub + 1;
-      } else {
-        nx.valid = cx.next_m0 >= 0;
-        nx.m0 = cx.next_m0;
-        nx.n0 = cx.next_n0;
-        nx.sub = 0;
-      }
-      if (nx.valid) {
-        mbar_arrive_expect_tx(&rbar[buf ^ 1], 16384);
-        tma_load_2d(sE + (buf ^ 1) * 16384, tmR, &rbar[buf ^ 1], nx.n0 + nx.sub * 32, nx.m0);
-      }
+    const int slot = cnt % R;
+    uint8_t* rb = wbase + slot * 4096;
+    uint8_t* ob = wbase + R * 4096 + (cnt % EpiCfg<BN, EPI_RESID>::NOB) * 2048;
+    const int col0 = n0 + sub * 32;
+    // column vectors first: their L2 latency overlaps the waits below
+    float4 bv[8], gv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      bv[j] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[j] = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
+                       : make_float4(1.f, 1.f, 1.f, 1.f);
     }
-    mbar_wait(&rbar[buf], (cnt >> 1) & 1);
+    if (lane == 0) {
+      // this warp's stores up to sub-tile cnt-1-(NOB-2) have read their smem, so the ring slot
+      // of sub-tile cnt+RAHEAD and the next bf16 buffer are free again
+      constexpr int AH = EpiCfg<BN, EPI_RESID>::RAHEAD;
+      bulk_wait_read<EpiCfg<BN, EPI_RESID>::NOB - 2>();
+      resid_issue<R>(rs, NS, cnt + AH, ew * 32, tmR, wbase, wbar);
+    }
+    mbar_wait(&wbar[slot], (cnt / R) & 1);
     uint32_t r[32];
     tmem_ld_x32(taddr + sub * 32, r);
     tmem_ld_wait();
@@ -259,15 +304,11 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
       __syncwarp();
       if (lane == 0) mbar_arrive_cl(tempty_cl);
     }
-    const int col0 = n0 + sub * 32;
     const uint32_t rbase = smem_u32(rb);
     float nv[32];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 g = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
-                                : make_float4(1.f, 1.f, 1.f, 1.f);
+      const float4 b = bv[j], g = gv[j];
       const uint32_t a = rbase + sw128(rit, j);
       const float4 x = ld_shared_f4(a);
       nv[4 * j + 0] = x.x + g.x * (__uint_as_float(r[4 * j + 0]) + b.x);
@@ -286,10 +327,10 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
                      pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
     }
     fence_async_smem();
-    epi_bar();
-    if (elected) {
-      tma_store_2d(tmR, rb, col0, m0);
-      if (ep.out2) tma_store_2d(tmO2, ob, col0, m0);
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmR, rb, col0, m0 + ew * 32);
+      if (ep.out2) tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
       bulk_commit();
     }
     ++cnt;
@@ -396,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kRBars);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -421,8 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
-      mbar_init(&rbar[i], 1);
     }
+    for (int i = 0; i < kRBars; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -494,19 +535,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int cnt = 0;
+    const ResidStream rs{(int)blockIdx.x, (int)gridDim.x, num_tiles, n_tiles, BM, 0};
     if constexpr (EPI == EPI_RESID) {
-      if (elected && (int)blockIdx.x < num_tiles) {  // first residual sub-tile
-        const int t0 = blockIdx.x;
-        mbar_arrive_expect_tx(&rbar[0], 16384);
-        tma_load_2d(sE, &tmR, &rbar[0], (t0 % n_tiles) * BN, (t0 / n_tiles) * BM);
+      constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
+      if (elected) {  // residual tiles 0 and 1 into L2
+        resid_prefetch_l2<BN>(rs, 0, &tmO);
+        resid_prefetch_l2<BN>(rs, 1, &tmO);
       }
+      if (lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
+        for (int j = 0; j < EpiCfg<BN, EPI>::RAHEAD; ++j)
+          resid_issue<R>(rs, BN / 32, j, ew * 32, &tmR, sE + ew * EpiCfg<BN, EPI>::WARP_BYTES, rbar + ew * R);
     }
+    int tix = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m0 = (tile / n_tiles) * BM;
       const int n0 = (tile % n_tiles) * BN;
-      const int nt = tile + gridDim.x;
-      cx.next_m0 = nt < num_tiles ? (nt / n_tiles) * BM : -1;
-      cx.next_n0 = nt < num_tiles ? (nt % n_tiles) * BN : 0;
+      if constexpr (EPI == EPI_RESID) {  // two tiles ahead: lands in L2 well before its epilogue
+        if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
+        ++tix;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
@@ -514,15 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       } else if constexpr (EPI == EPI_RESID) {
-        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, m0, n0, cx, elected, cnt, tcl,
-                           lane);
+        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected) bulk_wait<0>();
+    if (elected || (EPI == EPI_RESID && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -542,7 +588,7 @@ struct GemmCfg2 {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int BUDGET = 232448 - 1024 - BAR_BYTES - EpiCfg<BN, EPI>::BYTES;
   static constexpr int STAGES_RAW = BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
@@ -598,7 +644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kRBars);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -625,8 +671,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
-      mbar_init(&rbar[i], 1);
     }
+    for (int i = 0; i < kRBars; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -706,18 +752,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int cnt = 0;
+    const ResidStream rs{cid, nclusters, num_tiles, n_tiles, BM2, (int)rank * BM};
     if constexpr (EPI == EPI_RESID) {
-      if (elected && cid < num_tiles) {
-        mbar_arrive_expect_tx(&rbar[0], 16384);
-        tma_load_2d(sE, &tmR, &rbar[0], (cid % n_tiles) * BN, (cid / n_tiles) * BM2 + rank * BM);
+      constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
+      if (elected) {  // residual tiles 0 and 1 into L2
+        resid_prefetch_l2<BN>(rs, 0, &tmO);
+        resid_prefetch_l2<BN>(rs, 1, &tmO);
       }
+      if (lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
+        for (int j = 0; j < EpiCfg<BN, EPI>::RAHEAD; ++j)
+          resid_issue<R>(rs, BN / 32, j, ew * 32, &tmR, sE + ew * EpiCfg<BN, EPI>::WARP_BYTES, rbar + ew * R);
     }
+    int tix = 0;
     for (int tile = cid; tile < num_tiles; tile += nclusters) {
       const int m0 = (tile / n_tiles) * BM2 + rank * BM;
       const int n0 = (tile % n_tiles) * BN;
-      const int nt = tile + nclusters;
-      cx.next_m0 = nt < num_tiles ? (nt / n_tiles) * BM2 + rank * BM : -1;
-      cx.next_n0 = nt < num_tiles ? (nt % n_tiles) * BN : 0;
+      if constexpr (EPI == EPI_RESID) {  // two tiles ahead: lands in L2 well before its epilogue
+        if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
+        ++tix;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
@@ -725,15 +778,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       } else if constexpr (EPI == EPI_RESID) {
-        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, rit, m0, n0, cx, elected, cnt, tcl,
-                           lane);
+        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected) bulk_wait<0>();
+    if (elected || (EPI == EPI_RESID && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -855,12 +907,14 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
       break;
     case EPI_RESID:
       if (!ep.resid ||
-          make_tmap(&p->tmR, ep.resid, F32, 4, M, N, ep.ldr, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+          make_tmap(&p->tmR, ep.resid, F32, 4, M, N, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return -3;
       if (ep.out2 &&
-          make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+          make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
         return -3;
-      p->tmO = p->tmR;
+      // tmO (unused by this epilogue) carries the whole-tile map for the L2 prefetch
+      if (make_tmap(&p->tmO, ep.resid, F32, 4, M, N, ep.ldr, BM, bn, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return -3;
       if (!ep.out2) p->tmO2 = p->tmR;
       break;
     default:
