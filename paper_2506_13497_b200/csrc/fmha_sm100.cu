@@ -1,24 +1,30 @@
 // tcgen05 / TMEM flash attention (forward, non-causal, head_dim 72) for the STDiT3 spatial
 // and cross attention.
 //
-// One CTA = one (sequence, head, 128-query tile). Warp roles:
-//   warp 0     : TMA producer. Q/K/V come straight out of the token-major QKV (or q / kv)
-//                matrices through 4-D tensor maps {72, head slot, token, sequence}: the token
-//                dimension is clipped at the sequence length, so ragged tiles zero-fill on load
-//                and clip on store. head_dim 72 is split into a 64-column 128B-swizzled box and
-//                a 16-column 32B-swizzled box whose columns 72..79 fall outside the map (zeros).
-//   warp 1     : MMA issuer (one thread). S_j = Q K_j^T (M128 N128, K = 4 x16 SW128 + 1 x16 SW32)
-//                into a double-buffered TMEM S; O += P_j V_j with V as an MN-major B operand
-//                (N64 SW128 + N16 SW32, 8 k-steps of 16 keys) into TMEM O. QK_{j+1} is issued
-//                before PV_j so the tensor core computes the next scores while softmax runs.
-//   warps 4-7  : softmax, one query row per thread (= TMEM lane): online softmax in fp32 with
-//                exp2, lazy O rescaling (only when the running max grows by > 2^8), P written as
-//                bf16 into 128B-swizzled smem (the A operand of PV); final O / l -> bf16 -> smem
-//                -> TMA store.
-// Persistent: grid = #SMs, each CTA walks work items (q tile fastest); Q, K and V stream through
-// their own double-buffered rings across items, S / P / O are double-buffered, so the epilogue
-// (O / l -> TMA store) of item i overlaps the first tiles of item i+1.
-// TMEM: S0 [0,128), S1 [128,256), O0 [256,336), O1 [384,464) of a 512-column allocation.
+// One CTA = one work unit (sequence, head, PAIR of 128-query tiles); the two Q tiles ping-pong
+// on the tensor core so that one tile's softmax always overlaps the other tile's MMAs.
+// Warp roles (384 threads):
+//   warp 0      : TMA producer. Q/K/V come straight out of the token-major QKV (or q / kv)
+//                 matrices through 4-D tensor maps {72, head slot, token, sequence}: the token
+//                 dimension is clipped at the sequence length, so ragged tiles zero-fill on load
+//                 and clip on store. head_dim 72 is split into a 64-column 128B-swizzled box and
+//                 a 16-column 32B-swizzled box whose columns 72..79 fall outside the map (zeros).
+//   warps 1, 3  : MMA issuers (one thread each; warp 1 for Q tile 0, warp 3 for Q tile 1). Per
+//                 K/V tile j: S_g = Q_g K_j^T (M128 N128, K = 4 x16 SW128 + 1 x16 SW32) as soon
+//                 as group g holds S_{j-1} in registers, then O_g += P_g V_{j-1} (V as an MN-major
+//                 B operand, N64 SW128 + N16 SW32, 8 k-steps of 16 keys): the scores of tile j
+//                 are computed while the softmax of tile j-1 runs; the groups never wait on
+//                 each other.
+//   warp 2      : TMEM allocator.
+//   warps 4-7   : softmax of Q tile 0 of the unit, warps 8-11: of Q tile 1. One query row per
+//                 thread (= TMEM lane), all 128 keys of a tile in registers (setmaxnreg 200), so
+//                 no cross-warp exchange: online softmax in fp32 with exp2, lazy O rescaling
+//                 (only when the running max grows by > 2^8), P written as bf16 into
+//                 128B-swizzled smem (the A operand of PV); final O / l -> bf16 -> smem (the
+//                 tile's P buffer) -> TMA store.
+// Persistent: grid = #SMs, each CTA walks units (q-tile pair fastest, so concurrent CTAs share
+// K/V in L2); Q is double-buffered per softmax group, K and V stream through their own rings
+// across units. TMEM: S0 [0,128), S1 [128,256), O0 [256,336), O1 [384,464).
 #include "common.cuh"
 #include "ddit.h"
 #include "capi_internal.h"
@@ -26,24 +32,26 @@
 
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 namespace ddit {
 
 namespace fm {
 constexpr int BQ = 128, BKV = 128, THREADS = 384, KST = 2, VST = 2;
-constexpr int QA = 16384, QB = 4096;                 // Q: 64-col SW128 + 16-col SW32 boxes
+constexpr int QA = 16384, QB = 4096, QT = QA + QB;  // one Q tile: 64-col SW128 + 16-col SW32 boxes
 constexpr int KA = 16384, KB = 4096, VA = 16384, VB = 4096;
-constexpr int PBUF = 2 * 16384;                      // P: two 64-key SW128 regions
-constexpr int OFF_Q = 0;                             // 2 Q buffers
-constexpr int OFF_K = OFF_Q + 2 * (QA + QB);         // KST K stages
-constexpr int OFF_V = OFF_K + KST * (KA + KB);       // VST V stages
-constexpr int OFF_P = OFF_V + VST * (VA + VB);       // 2 P buffers
-constexpr int OFF_OST = OFF_P + 2 * PBUF;            // O staging (128 x 144 B)
-constexpr int OFF_BAR = OFF_OST + 128 * 144;
-constexpr int SMEM = 1024 + OFF_BAR + 26 * 8 + 3072;
-constexpr uint32_t TM_S0 = 0, TM_S1 = 128, TM_O0 = 256, TM_O1 = 384;
+constexpr int PBUF = 2 * 16384;                    // P of one Q tile: two 64-key SW128 regions
+constexpr int OFF_Q = 0;                           // [2 groups][2 buffers] Q tiles
+constexpr int OFF_K = OFF_Q + 4 * QT;              // KST K stages
+constexpr int OFF_V = OFF_K + KST * (KA + KB);     // VST V stages
+constexpr int OFF_P = OFF_V + VST * (VA + VB);     // P per group (also its O store staging)
+constexpr int OFF_BAR = OFF_P + 2 * PBUF;
+constexpr int NBAR = 28;
+constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
+constexpr uint32_t TM_S0 = 0, TM_O0 = 256;  // group g: S at TM_S0 + 128 g, O at TM_O0 + 128 g
 constexpr float RESCALE_LOG2 = 8.0f;
+static_assert(SMEM <= 232448, "fmha smem");
 }  // namespace fm
 
 
@@ -165,12 +173,32 @@ DDIT_DEV float fmax3(float a, float b, float c) {
 DDIT_DEV void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// Two 2^x on the FMA pipe (x <= ~8; clamped at -127): round-to-nearest split x = j + f through the
+// 1.5 * 2^23 magic add, f in [-0.5, 0.5], cubic minimax p(f) (rel. err 1.4e-4 << bf16 ulp), then j
+// added into the exponent field with one integer op -- offloads part of the exps from MUFU.
+DDIT_DEV float2 exp2_poly_x2(float x0, float x1) {
+  const float2 x = make_float2(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(make_float2(0.05502926645f, 0.05502926645f), f,
+                        make_float2(0.24225698193f, 0.24225698193f));
+  q = __ffma2_rn(q, f, make_float2(0.69325305500f, 0.69325305500f));
+  q = __ffma2_rn(q, f, make_float2(0.99995133866f, 0.99995133866f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+// chunks (8 keys each) of a full tile whose exps run on the FMA pipe instead of MUFU: every
+// POLY-th chunk (POLY = 0: none)
+template <int POLY>
+__host__ __device__ constexpr bool poly_chunk(int c) { return POLY > 0 && c % POLY == POLY - 1; }
 DDIT_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
+template <int POLY>
 __global__ void __launch_bounds__(fm::THREADS, 1)
     fmha_sm100_kernel(const __grid_constant__ CUtensorMap tmQa,
                       const __grid_constant__ CUtensorMap tmQb,
@@ -183,24 +211,23 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fm_smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint64_t* q_full = bars + 0;    // [2]
-  uint64_t* q_empty = bars + 2;   // [2]
-  uint64_t* k_full = bars + 4;    // [KST]
-  uint64_t* k_empty = bars + 6;   // [KST]
-  uint64_t* v_full = bars + 8;    // [VST]
-  uint64_t* v_empty = bars + 10;  // [VST]
-  uint64_t* s_full = bars + 12;   // [2]
-  uint64_t* s_free = bars + 14;   // [2]
-  uint64_t* p_full = bars + 16;   // [2]
-  uint64_t* pv_done = bars + 18;  // [2]
-  uint64_t* o_full = bars + 20;   // [2]
-  uint64_t* o_free = bars + 22;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-  float* xmax = reinterpret_cast<float*>(bars + 26);  // [2 tile parity][2][128] partial row maxima, [2][128] row sums
+  uint64_t* q_full = bars + 0;    // [group * 2 + buffer]
+  uint64_t* q_empty = bars + 4;   // [group * 2 + buffer]
+  uint64_t* k_full = bars + 8;    // [KST]
+  uint64_t* k_empty = bars + 10;  // [KST]
+  uint64_t* v_full = bars + 12;   // [VST]
+  uint64_t* v_empty = bars + 14;  // [VST]
+  uint64_t* s_full = bars + 16;   // [group]
+  uint64_t* s_free = bars + 18;   // [group]
+  uint64_t* p_full = bars + 20;   // [group]
+  uint64_t* pv_done = bars + 22;  // [group]
+  uint64_t* o_free = bars + 24;   // [group]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = warp_id(), lane = lane_id();
   const int nk = (p.Lk + BKV - 1) / BKV;
-  const int n_items = p.q_tiles * p.heads * p.seqs;
+  const int pairs = (p.q_tiles + 1) >> 1;
+  const int n_units = pairs * p.heads * p.seqs;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQa);
@@ -208,19 +235,20 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
     tma_prefetch_desc(&tmKVa);
     tma_prefetch_desc(&tmKVb);
     tma_prefetch_desc(&tmO);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+      mbar_init(&k_empty[i], 2);  // released by both groups' MMA warps
       mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init(&v_empty[i], 2);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 8);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], 8);
+      mbar_init(&o_free[i], 4);
     }
     fence_barrier_init();
   }
@@ -231,25 +259,33 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
 
-  // work item -> (q tile, head, sequence); q tile fastest so concurrent CTAs share K/V in L2
-  auto decode = [&](int wi, int& qt, int& head, int& seq) {
-    qt = wi % p.q_tiles;
-    head = (wi / p.q_tiles) % p.heads;
-    seq = wi / (p.q_tiles * p.heads);
+  // unit -> (q-tile pair, head, sequence); pair fastest so concurrent CTAs share K/V in L2
+  auto decode = [&](int u, int& pr, int& head, int& seq, bool& has1) {
+    pr = u % pairs;
+    head = (u / pairs) % p.heads;
+    seq = u / (pairs * p.heads);
+    has1 = 2 * pr + 1 < p.q_tiles;
   };
 
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ TMA producer
-      int kc = 0, vc = 0, it = 0;
-      for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it) {
-        int qt, head, seq;
-        decode(wi, qt, head, seq);
-        const int qb = it & 1;
-        mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
-        uint8_t* qbuf = sm + OFF_Q + qb * (QA + QB);
-        mbar_arrive_expect_tx(&q_full[qb], QA + QB);
-        tma_load_4d(qbuf, &tmQa, &q_full[qb], 0, p.q_slot + head, qt * BQ, seq);
-        tma_load_4d(qbuf + QA, &tmQb, &q_full[qb], 64, p.q_slot + head, qt * BQ, seq);
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
+    if (warp == 0 && lane == 0) {  // ------------------------------------------ TMA producer
+      int kc = 0, vc = 0, qc[2] = {0, 0};
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pr, head, seq;
+        bool has1;
+        decode(u, pr, head, seq, has1);
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (g == 1 && !has1) break;
+          const int qi = g * 2 + (qc[g] & 1);
+          mbar_wait(&q_empty[qi], ((qc[g] >> 1) & 1) ^ 1);
+          uint8_t* qbuf = sm + OFF_Q + qi * QT;
+          mbar_arrive_expect_tx(&q_full[qi], QT);
+          tma_load_4d(qbuf, &tmQa, &q_full[qi], 0, p.q_slot + head, (2 * pr + g) * BQ, seq);
+          tma_load_4d(qbuf + QA, &tmQb, &q_full[qi], 64, p.q_slot + head, (2 * pr + g) * BQ, seq);
+          ++qc[g];
+        }
         for (int j = 0; j < nk; ++j, ++kc, ++vc) {
           const int ks = kc % KST, vs = vc % VST;
           mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
@@ -265,119 +301,126 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         }
       }
       pdl_trigger();
-    }
-  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
-    constexpr uint32_t id_qk = idesc_f16(128, 128, false);
-    constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
-    constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
-    int kc = 0, vc = 0, t0 = 0, it = 0;
-    for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it, t0 += nk) {
-      const int qb = it & 1, ob = it & 1;
-      const uint32_t qa = smem_u32(sm + OFF_Q + qb * (QA + QB)), qbb = qa + QA;
-      const uint32_t o_tm = tmem + (ob ? TM_O1 : TM_O0);
-      mbar_wait(&q_full[qb], (it >> 1) & 1);
-      mbar_wait(&o_free[ob], ((it >> 1) & 1) ^ 1);
-      auto issue_qk = [&](int t) {  // S[t & 1] = Q K^T for global tile t
-        const int ks = kc % KST;
-        mbar_wait(&k_full[ks], (kc / KST) & 1);
-        if (t >= 2) mbar_wait(&s_free[t & 1], ((t - 2) >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t ka = smem_u32(sm + OFF_K + ks * (KA + KB)), kb = ka + KA;
-          const uint32_t d = tmem + ((t & 1) ? TM_S1 : TM_S0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16_ss(d, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2), id_qk,
-                         k > 0);
-          umma_bf16_ss(d, sdesc(qbb, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
-          umma_commit(&s_full[t & 1]);
-          umma_commit(&k_empty[ks]);
-        }
-        __syncwarp();
-        ++kc;
-      };
-      tc_fence_after();
-      issue_qk(t0);
-      for (int j = 0; j < nk; ++j) {
-        const int t = t0 + j;
-        if (j + 1 < nk) issue_qk(t + 1);
-        const int vs = vc % VST;
-        mbar_wait(&p_full[t & 1], (t >> 1) & 1);
-        mbar_wait(&v_full[vs], (vc / VST) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t va = smem_u32(sm + OFF_V + vs * (VA + VB)), vb = va + VA;
-          const uint32_t pb = smem_u32(sm + OFF_P + (t & 1) * PBUF);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
-            const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
-            umma_bf16_ss(o_tm, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
-            umma_bf16_ss(o_tm + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+    } else if (warp == 1 || warp == 3) {  // ------------------------ MMA issuers, one per group
+      // Each softmax group has its own issuing warp (warp 1: group 0, warp 3: group 1), so a
+      // group's QK / PV go to the tensor core as soon as ITS softmax is ready, independent of the
+      // other group's progress; the shared K / V stages are released by both (count-2 barriers).
+      const int g = warp == 1 ? 0 : 1;
+      constexpr uint32_t id_qk = idesc_f16(128, 128, false);
+      constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
+      constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
+      const uint32_t s_tmem = tmem + TM_S0 + 128 * g, o_tmem = tmem + TM_O0 + 128 * g;
+      const uint32_t pb = smem_u32(sm + OFF_P + g * PBUF);
+      int kc = 0, vc = 0, qc = 0, sn = 0, pn = 0, un = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pr, head, seq;
+        bool has1;
+        decode(u, pr, head, seq, has1);
+        if (g == 1 && !has1) {  // no second Q tile: keep the shared K / V ring in step
+          for (int j = 0; j < nk; ++j, ++kc, ++vc) {
+            mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
+            if (lane == 0) mbar_arrive(&k_empty[kc % KST]);
+            mbar_wait(&v_full[vc % VST], (vc / VST) & 1);
+            if (lane == 0) mbar_arrive(&v_empty[vc % VST]);
+            __syncwarp();
           }
-          umma_commit(&pv_done[t & 1]);
-          umma_commit(&v_empty[vs]);
-          if (j == nk - 1) {
-            umma_commit(&q_empty[qb]);
-            umma_commit(&o_full[ob]);
+          continue;
+        }
+        const int qi = g * 2 + (qc & 1);
+        const uint32_t qa = smem_u32(sm + OFF_Q + qi * QT);
+        mbar_wait(&q_full[qi], (qc >> 1) & 1);
+        if (un > 0) mbar_wait(&o_free[g], (un - 1) & 1);  // the group read its previous O
+        for (int j = 0; j <= nk; ++j) {
+          if (j < nk) {  // S = Q K_j^T once the group holds its previous S in registers
+            mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
+            if (sn > 0) mbar_wait(&s_free[g], (sn - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t ka = smem_u32(sm + OFF_K + (kc % KST) * (KA + KB)), kb = ka + KA;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                umma_bf16_ss(s_tmem, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2),
+                             id_qk, k > 0);
+              umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
+              umma_commit(&s_full[g]);
+              umma_commit(&k_empty[kc % KST]);
+              if (j == nk - 1) umma_commit(&q_empty[qi]);
+            }
+            __syncwarp();
+            ++sn;
+            ++kc;
+          }
+          if (j > 0) {  // O (+)= P_{j-1} V_{j-1} once the group wrote P
+            mbar_wait(&v_full[vc % VST], (vc / VST) & 1);
+            mbar_wait(&p_full[g], pn & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t va = smem_u32(sm + OFF_V + (vc % VST) * (VA + VB)), vb = va + VA;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+                const uint32_t acc = (j > 1 || kk > 0) ? 1u : 0u;
+                umma_bf16_ss(o_tmem, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
+                umma_bf16_ss(o_tmem + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+              }
+              umma_commit(&pv_done[g]);
+              umma_commit(&v_empty[vc % VST]);
+            }
+            __syncwarp();
+            ++pn;
+            ++vc;
           }
         }
-        __syncwarp();
-        ++vc;
+        ++qc;
+        ++un;
       }
     }
-  } else if (warp >= 4) {  // ------------------------------------------ softmax
-    // 8 warps: warp w covers TMEM lanes 32*(w%4).. (query rows) and key half h = (w-4)/4 of
-    // every S tile (64 of the 128 columns); the two halves of a row exchange their partial
-    // max through smem under a 64-thread named barrier (one per lane quarter).
+  } else {  // ------------------------------------------------------------ softmax groups
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    const int g = (warp - 4) >> 2;
     const int quarter = warp & 3;
-    const int half = (warp - 4) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const int bar_id = 2 + quarter;
-    const bool elected = warp == 4 && lane == 0;
-    int pv_known = -1;  // highest global tile whose PV is known complete
-    int t0 = 0, it = 0;
-    for (int wi = blockIdx.x; wi < n_items; wi += gridDim.x, ++it, t0 += nk) {
-      int qt, head, seq;
-      decode(wi, qt, head, seq);
-      const int ob = it & 1;
-      const uint32_t o_tm = lane_base + (ob ? TM_O1 : TM_O0);
+    const uint32_t s_tm = lane_base + TM_S0 + 128 * g, o_tm = lane_base + TM_O0 + 128 * g;
+    const int bar_id = 1 + g;
+    const bool elected = quarter == 0 && lane == 0;
+    uint8_t* pbuf = sm + OFF_P + g * PBUF;
+    int n = 0;  // tiles processed by this group
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int pr, head, seq;
+      bool has1;
+      decode(u, pr, head, seq, has1);
+      if (g == 1 && !has1) continue;
+      const int qt = 2 * pr + g;
       float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < nk; ++j) {
-        const int t = t0 + j;
-        mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+      for (int j = 0; j < nk; ++j, ++n) {
+        mbar_wait(&s_full[g], n & 1);
         tc_fence_after();
-        uint32_t s[64];
-        const uint32_t sadr = lane_base + ((t & 1) ? TM_S1 : TM_S0) + half * 64;
-        tmem_ld32(sadr, s);
-        tmem_ld32(sadr + 32, s + 32);
+        uint32_t s[128];
+        tmem_ld32(s_tm, s);
+        tmem_ld32(s_tm + 32, s + 32);
+        tmem_ld32(s_tm + 64, s + 64);
+        tmem_ld32(s_tm + 96, s + 96);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[t & 1]);
-        const int valid = min(BKV, p.Lk - j * BKV) - half * 64;  // may be <= 0
+        if (lane == 0) mbar_arrive(&s_free[g]);
+        const int valid = min(BKV, p.Lk - j * BKV);
+        const bool full = valid == BKV;
         float mx8[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-        const bool full = valid >= 64;  // every tile but the ragged last one
+        for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
         if (full) {
 #pragma unroll
-          for (int e = 0; e < 64; e += 2)
+          for (int e = 0; e < 128; e += 2)
             mx8[(e >> 1) & 7] = fmax3(mx8[(e >> 1) & 7], __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
         } else {
 #pragma unroll
-          for (int e = 0; e < 64; ++e)
+          for (int e = 0; e < 128; ++e)
             if (e < valid) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(s[e]));
         }
-        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        // tile-parity slots: the partner's read of slot t&1 precedes its arrival at tile t+1's
-        // barrier, so slot t&1 is free again at tile t+2 -- one barrier per tile
-        float* xm = xmax + (t & 1) * 256;
-        xm[half * 128 + row] = mx;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float m_new = fmaxf(m, mx * p.scale_log2);
         const bool resc = m_new > m + RESCALE_LOG2;
         float alpha = 1.f;
@@ -386,60 +429,37 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           m = m_new;
           l *= alpha;
         }
-        if (j > 0 && __any_sync(0xffffffffu, resc)) {
-          if (pv_known < t - 1) {
-            mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
-            pv_known = t - 1;
-          }
-          tc_fence_after();
-          if (half == 0) {  // O columns [0, 64)
-            uint32_t o[64];
-            tmem_ld32(o_tm, o);
-            tmem_ld32(o_tm + 32, o + 32);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 64; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(o_tm, o);
-            tmem_st32(o_tm + 32, o + 32);
-          } else {  // O columns [64, 80)
-            uint32_t o[16];
-            tmem_ld16(o_tm + 64, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st16(o_tm + 64, o);
-          }
-          tmem_st_wait();
-        }
-        if (t >= 2 && pv_known < t - 2) {  // P buffer (t & 1) was read by PV_{t-2}
-          mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);
-          pv_known = t - 2;
-        }
-        const uint32_t pbase = smem_u32(sm + OFF_P + (t & 1) * PBUF) + half * 16384;
+        // exps first (packed bf16 P kept in the consumed s[] registers: chunk c -> s[4c..4c+3]),
+        // so the MUFU work overlaps the tensor core finishing PV_{j-1}
         const float neg_m = -m;
         float rs8[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) rs8[u] = 0.f;
-        const uint32_t prow = pbase + (uint32_t)(row * 128);
+        for (int e = 0; e < 8; ++e) rs8[e] = 0.f;
         if (full) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {  // 8 chunks of 8 keys (one 128 B swizzled row)
+          for (int c = 0; c < 16; ++c) {
             float pv[8];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               float x0, x1;
               ffma2(x0, x1, __uint_as_float(s[c * 8 + e]), __uint_as_float(s[c * 8 + e + 1]),
                     p.scale_log2, neg_m);
-              pv[e] = fast_exp2(x0);
-              pv[e + 1] = fast_exp2(x1);
+              if (poly_chunk<POLY>(c)) {
+                const float2 y = exp2_poly_x2(x0, x1);
+                pv[e] = y.x;
+                pv[e + 1] = y.y;
+              } else {
+                pv[e] = fast_exp2(x0);
+                pv[e + 1] = fast_exp2(x1);
+              }
               fadd2(rs8[e], rs8[e + 1], pv[e], pv[e + 1]);
             }
-            st_shared_u4(prow + ((c ^ (row & 7)) << 4), pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
-                         pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 16; ++c) {
             float pv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -447,51 +467,66 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
               pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
               rs8[e] += pv[e];
             }
-            st_shared_u4(prow + ((c ^ (row & 7)) << 4), pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]),
-                         pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
         }
+        if (j > 0) {
+          // PV of the previous tile done: P buffer free, O complete through tile j-1
+          mbar_wait(&pv_done[g], (n - 1) & 1);
+          if (__any_sync(0xffffffffu, resc)) {
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < 80; c += 16) {  // 16 columns at a time
+              uint32_t o[16];
+              tmem_ld16(o_tm + c, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st16(o_tm + c, o);
+            }
+            tmem_st_wait();
+          }
+        } else {
+          // the P buffer staged the previous unit's O store: wait until the TMA read it
+          if (elected) bulk_wait_read0();
+          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        }
+        const uint32_t prow = smem_u32(pbuf) + (uint32_t)(row * 128);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)  // chunk c (8 keys) -> region c / 8, 16 B swizzled
+          st_shared_u4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), s[4 * c], s[4 * c + 1],
+                       s[4 * c + 2], s[4 * c + 3]);
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t & 1]);
+        if (lane == 0) mbar_arrive(&p_full[g]);
       }
-      // ---- item epilogue: O / l -> bf16 -> staging smem (144 B rows) -> TMA store
-      mbar_wait(&o_full[ob], (it >> 1) & 1);
-      pv_known = t0 + nk - 1;
+      // ---- unit epilogue: O / l -> bf16 -> staging (the P buffer, 144 B rows) -> TMA store
+      mbar_wait(&pv_done[g], (n - 1) & 1);
       tc_fence_after();
-      uint32_t o[40];  // half 0: output columns [0, 40), half 1: [40, 72)
-      if (half == 0) {
-        tmem_ld32(o_tm, o);
-        tmem_ld_32x32b_x8_fm(o_tm + 32, o + 32);
-      } else {
-        tmem_ld32(o_tm + 40, o);
-      }
+      uint32_t o[72];
+      tmem_ld32(o_tm, o);
+      tmem_ld32(o_tm + 32, o + 32);
+      tmem_ld_32x32b_x8_fm(o_tm + 64, o + 64);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[ob]);
-      xmax[512 + half * 128 + row] = l;
-      if (elected) bulk_wait_read0();  // previous item's store no longer reads the staging
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      const float lt = l + xmax[512 + (half ^ 1) * 128 + row];
-      const float inv = lt > 0.f ? 1.f / lt : 0.f;
-      const uint32_t obase = smem_u32(sm + OFF_OST) + row * 144;
-      const int c0 = half ? 5 : 0, nc = half ? 4 : 5;
+      if (lane == 0) mbar_arrive(&o_free[g]);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const uint32_t obase = smem_u32(pbuf) + row * 144;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        if (c < nc)
-          st_shared_u4(obase + (c0 + c) * 16,
-                       pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
-                       pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
-                       pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
-                       pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
-      }
+      for (int c = 0; c < 9; ++c)
+        st_shared_u4(obase + c * 16,
+                     pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+                     pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+                     pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+                     pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // staging written; xmax reusable
+      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       if (elected) {
-        tma_store_4d(&tmO, sm + OFF_OST, 0, p.o_slot + head, qt * BQ, seq);
+        tma_store_4d(&tmO, pbuf, 0, p.o_slot + head, qt * BQ, seq);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
@@ -591,20 +626,39 @@ int fmha_plan_init(FmhaPlan* fp, const ddit_attn* a) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int items = fp->p.q_tiles * a->heads * a->num_seqs;
-  fp->grid = dim3(items < sms ? items : sms, 1, 1);
+  const int units = ((fp->p.q_tiles + 1) / 2) * a->heads * a->num_seqs;
+  fp->grid = dim3(units < sms ? units : sms, 1, 1);
   return DDIT_OK;
 }
 
-int fmha_plan_launch(const FmhaPlan* fp, cudaStream_t s) {
+static int fmha_poly() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DDIT_FMHA_POLY");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
+template <int POLY>
+static int fmha_launch_t(const FmhaPlan* fp, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fmha_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
+    cudaFuncSetAttribute(fmha_sm100_kernel<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
     attr = true;
   }
-  launch_pdl(fmha_sm100_kernel, fp->grid, dim3(fm::THREADS), fm::SMEM, s, fp->tmQa, fp->tmQb,
+  launch_pdl(fmha_sm100_kernel<POLY>, fp->grid, dim3(fm::THREADS), fm::SMEM, s, fp->tmQa, fp->tmQb,
              fp->tmKVa, fp->tmKVb, fp->tmO, fp->p);
   return check_cuda("fmha_sm100_kernel");
+}
+
+int fmha_plan_launch(const FmhaPlan* fp, cudaStream_t s) {
+  switch (fmha_poly()) {
+    case 0: return fmha_launch_t<0>(fp, s);
+    case 2: return fmha_launch_t<2>(fp, s);
+    case 3: return fmha_launch_t<3>(fp, s);
+    default: return fmha_launch_t<4>(fp, s);
+  }
 }
 
 }  // namespace ddit
