@@ -49,6 +49,20 @@ def latent_gather(dst: torch.Tensor, t_lo: int, t_hi: int, sources: list[tuple[t
     check(lib().ddit_latent_gather(dst.data_ptr(), t_lo, t_hi, P, lo, hi, n, C, HW, stream_ptr(stream)))
 
 
+def exchange_bytes(sh: VideoShape, P: int, rank: int, C: int, B: int = 2) -> int:
+    """Bytes rank ``rank`` of a DoP-P group pushes to its peers in one step: 28 spatial->temporal
+    exchanges (its T-shard rows outside its own S-shard) + 28 temporal->spatial ones (its S-shard
+    rows outside its own T-shard), fp32 residual rows of C channels, CFG batch B."""
+    if P == 1:
+        return 0
+    from .shapes import s_shard, t_shard
+
+    t_lo, t_hi = t_shard(sh, P, rank)
+    s_lo, s_hi = s_shard(sh, P, rank)
+    Tl, Sl = t_hi - t_lo, s_hi - s_lo
+    return 28 * (B * Tl * (sh.S - Sl) * C * 4 + B * (sh.T - Tl) * Sl * C * 4)
+
+
 @dataclass
 class _Live:
     """One request's device state on its current group."""
@@ -67,7 +81,8 @@ class B200Executor:
     def __init__(self, cfg: STDiTConfig, weights: dict[str, torch.Tensor], *,
                  shapes: dict[str, VideoShape] | None = None, num_steps: int = 30,
                  guidance: float = 7.0, seed_base: int = 0, vae_cfg=None, vae_weights=None,
-                 keep_videos: bool = False):
+                 keep_videos: bool = False, emulate_group: bool = False,
+                 nvlink_gbs: float = 770.0):
         self.cfg = cfg
         self.ndev = max(torch.cuda.device_count(), 1)
         self.models: dict[int, STDiTModel] = {}
@@ -86,6 +101,12 @@ class B200Executor:
         self.keep_videos = keep_videos
         self.videos: dict[int, torch.Tensor] = {}
         self.vae_seconds: list[tuple[int, float, float]] = []  # (request, handoff s, decode s)
+        # A group whose ranks share one device normally reports the whole group's time on that
+        # device. With emulate_group it reports the DoP-P step latency the group would have on P
+        # GPUs: max over ranks of each rank's own device time + its exchange bytes over NVLink
+        # (measured 770 GB/s peer copy), so one B200 can replay an 8-GPU trace.
+        self.emulate_group = emulate_group
+        self.nvlink_gbs = nvlink_gbs
 
     # ---------------------------------------------------------------- helpers
     def device_of(self, gpu_id: int) -> int:
@@ -209,6 +230,13 @@ class B200Executor:
     # ---------------------------------------------------------------- internals
     def _run_step(self, live: _Live, step: int) -> float:
         step = min(step, self.num_steps - 1)
+        if live.group is not None and self.emulate_group and len(live.ranks) > 1:
+            with torch.cuda.device(live.shards[0].device):
+                per_rank = live.group.step_timed(live.shards, step)
+            sh = live.ranks[0].shape
+            P = len(live.ranks)
+            xb = max(exchange_bytes(sh, P, r, self.cfg.hidden) for r in range(P))
+            return max(per_rank) / 1e3 + xb / (self.nvlink_gbs * 1e9)
         if live.group is not None:
             dev = live.shards[0].device
             with torch.cuda.device(dev):

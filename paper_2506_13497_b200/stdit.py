@@ -254,6 +254,35 @@ class VirtualGroup:
         return z_parts
 
 
+    def step_timed(self, z_parts: list[torch.Tensor], step: int) -> list[float]:
+        """The same lockstep step with a CUDA-event pair around every rank's share of each phase
+        (its kernels and its exchange pushes). Returns per-rank device ms: what each rank's GPU
+        spends on the step when the ranks run on P GPUs (cross-rank waiting excluded)."""
+        s = torch.cuda.current_stream()
+
+        def ev():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            return e
+
+        spans: list[list[tuple]] = [[] for _ in self.ranks]
+        for i, (r, z) in enumerate(zip(self.ranks, z_parts)):
+            a = ev()
+            r.begin(z, step)
+            spans[i].append((a, ev()))
+        for k in range(2 * self.depth):
+            for i, r in enumerate(self.ranks):
+                a = ev()
+                r.phase(k)
+                spans[i].append((a, ev()))
+        for i, (r, z) in enumerate(zip(self.ranks, z_parts)):
+            a = ev()
+            r.end(z, step)
+            spans[i].append((a, ev()))
+        s.synchronize()
+        return [sum(a.elapsed_time(b) for a, b in sp) for sp in spans]
+
+
 def launch_count() -> int:
     """Kernel launches issued by libddit in this process (bench evidence)."""
     return int(lib().ddit_launch_count())

@@ -23,22 +23,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 
 from paper_2506_13497_b200 import shapes, weights
+from paper_2506_13497_b200.executor import exchange_bytes
 from paper_2506_13497_b200.stdit import STDiTModel, StepRequest, VirtualGroup
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-
-
-def exchange_bytes(sh, P: int, rank: int, C: int, B: int = 2) -> int:
-    """Bytes rank `rank` pushes to other ranks per step: 28 sp->tp (its T-shard rows outside its
-    own S-shard) + 28 tp->sp (its S-shard rows outside its own T-shard), fp32 residual rows."""
-    if P == 1:
-        return 0
-    t_lo, t_hi = shapes.t_shard(sh, P, rank)
-    s_lo, s_hi = shapes.s_shard(sh, P, rank)
-    Tl, Sl = t_hi - t_lo, s_hi - s_lo
-    sp2tp = B * Tl * (sh.S - Sl) * C * 4
-    tp2sp = B * (sh.T - Tl) * Sl * C * 4
-    return 28 * (sp2tp + tp2sp)
 
 
 def ev_time(fn, reps: int) -> float:
