@@ -859,11 +859,45 @@ int num_sms() {
 
 static bool bn_ok(int bn, int epi) {
   if (epi == EPI_QKV) return bn == 144;
+  if (bn == 0) return false;
   return bn == 96 || bn == 128 || bn == 192 || bn == 256;
 }
 
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
                    int K, int epi, const EpiParams& ep, int bn) {
+  return gemm_plan_init_cta(p, A, lda, B, ldb, M, N, K, epi, ep, bn, two_cta_enabled() ? 1 : 0);
+}
+
+// Tile choice for an M x N output on this GPU: fewest "tile-waves" weighted by the per-tile
+// efficiency measured at large M (240p, K = 1152) -- 2-CTA 256 x BN tiles over #SMs/2 pairs,
+// 1-CTA 128 x BN tiles over #SMs. Only M/N tiling changes (never the K order), so every choice
+// gives bit-identical results: a DoP-P rank with a small M may pick a different tile than DoP 1.
+void gemm_pick_tile(int M, int N, int epi, int* bn_out, int* two_out) {
+  struct Cand { int bn, two; double eff; };
+  static const Cand cands[] = {{256, 1, 1.0}, {192, 1, 1.0},  {144, 1, 1.0},  {128, 1, 0.90},
+                               {96, 1, 0.72}, {256, 0, 0.85}, {192, 0, 0.85}, {144, 0, 0.85},
+                               {128, 0, 0.74}, {96, 0, 0.62}};
+  const int sms = num_sms();
+  double best = 1e30;
+  int bbn = 0, btwo = 0;
+  for (const Cand& c : cands) {
+    if (c.two && !two_cta_enabled()) continue;
+    if ((epi == EPI_QKV) != (c.bn == 144) || N % c.bn) continue;
+    const int bm = c.two ? 2 * BM : BM, units = c.two ? sms / 2 : sms;
+    const long tiles = (long)((M + bm - 1) / bm) * (N / c.bn);
+    const double cost = (double)((tiles + units - 1) / units) * c.bn / c.eff;
+    if (cost < best - 1e-9) {
+      best = cost;
+      bbn = c.bn;
+      btwo = c.two;
+    }
+  }
+  *bn_out = bbn;
+  *two_out = btwo;
+}
+
+int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
+                       int K, int epi, const EpiParams& ep, int bn, int two_cta) {
   if (!bn_ok(bn, epi)) {
     snprintf(g_err, sizeof g_err, "unsupported BN %d for epilogue %d", bn, epi);
     return -2;
@@ -882,7 +916,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, 
     return -2;
   }
   memset(p, 0, sizeof *p);
-  p->two_cta = two_cta_enabled() ? 1 : 0;
+  p->two_cta = two_cta ? 1 : 0;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   if (make_tmap(&p->tmA, A, BF, 2, M, K, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return -3;

@@ -56,6 +56,10 @@ struct GemmPlan {
 // Build the TMA descriptors and launch geometry. Returns 0 on success.
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
                    int K, int epi, const EpiParams& ep, int bn);
+int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N,
+                       int K, int epi, const EpiParams& ep, int bn, int two_cta);
+// BN and 1-/2-CTA tiles for an M x N output (fills the GPU at small M; bit-identical results)
+void gemm_pick_tile(int M, int N, int epi, int* bn, int* two_cta);
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
 int num_sms();
 bool two_cta_enabled();

@@ -220,14 +220,20 @@ int pick_bn(int n) {
   return 0;
 }
 
+// block GEMM plan with the tile chosen for this rank's M (gemm_pick_tile)
+int plan_auto(GemmPlan* p, const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+              int epi, const EpiParams& e) {
+  int bn = 0, two = 0;
+  gemm_pick_tile(M, N, epi, &bn, &two);
+  return gemm_plan_init_cta(p, A, lda, B, ldb, M, N, K, epi, e, bn, two);
+}
+
 int build_plans(ddit_req* r) {
   const ddit_config& c = r->m->cfg;
   const Geometry& g = r->g;
   const int C = c.hidden;
   const int nblk = 2 * c.depth;
   r->plans.assign((size_t)nblk * G_N, GemmPlan{});
-  const int bn_c = pick_bn(C);
-  const int bn_mlp = c.mlp_hidden % 256 == 0 ? 256 : pick_bn(c.mlp_hidden);
   for (int k = 0; k < nblk; ++k) {
     const bool temporal = k & 1;
     const int M = temporal ? g.M_tp : g.M_sp;
@@ -253,7 +259,7 @@ int build_plans(ddit_req* r) {
     e.rope_tab = reinterpret_cast<const float2*>(r->rope);
     e.eps = c.eps;
     e.rows_per_b = rpb;
-    if ((rc = gemm_plan_init(&P[G_QKV], r->xm, C, bw.qkv_w, C, M, 3 * C, C, EPI_QKV, e, 144)))
+    if ((rc = plan_auto(&P[G_QKV], r->xm, C, bw.qkv_w, C, M, 3 * C, C, EPI_QKV, e)))
       return rc;
     // attention out-projection: x += gate_msa * (.) ; bf16 copy of x for cross-attn queries
     memset(&e, 0, sizeof e);
@@ -265,7 +271,7 @@ int build_plans(ddit_req* r) {
     e.rows_per_b = rpb;
     e.out2 = r->xb;
     e.ldo2 = C;
-    if ((rc = gemm_plan_init(&P[G_PROJ], r->ao, C, bw.proj_w, C, M, C, C, EPI_RESID, e, bn_c)))
+    if ((rc = plan_auto(&P[G_PROJ], r->ao, C, bw.proj_w, C, M, C, C, EPI_RESID, e)))
       return rc;
     // cross-attn queries
     memset(&e, 0, sizeof e);
@@ -273,14 +279,14 @@ int build_plans(ddit_req* r) {
     e.out = r->xm;
     e.ldo = C;
     e.rows_per_b = rpb;
-    if ((rc = gemm_plan_init(&P[G_CQ], r->xb, C, bw.cq_w, C, M, C, C, EPI_BF16, e, bn_c))) return rc;
+    if ((rc = plan_auto(&P[G_CQ], r->xb, C, bw.cq_w, C, M, C, C, EPI_BF16, e))) return rc;
     // cross-attn out projection: x += (.)
     memset(&e, 0, sizeof e);
     e.bias = bw.cproj_b;
     e.resid = x;
     e.ldr = C;
     e.rows_per_b = rpb;
-    if ((rc = gemm_plan_init(&P[G_CPROJ], r->ao, C, bw.cproj_w, C, M, C, C, EPI_RESID, e, bn_c)))
+    if ((rc = plan_auto(&P[G_CPROJ], r->ao, C, bw.cproj_w, C, M, C, C, EPI_RESID, e)))
       return rc;
     // MLP
     memset(&e, 0, sizeof e);
@@ -288,8 +294,7 @@ int build_plans(ddit_req* r) {
     e.out = r->big;
     e.ldo = c.mlp_hidden;
     e.rows_per_b = rpb;
-    if ((rc = gemm_plan_init(&P[G_FC1], r->xm, C, bw.fc1_w, C, M, c.mlp_hidden, C, EPI_GELU_BF16, e,
-                             bn_mlp)))
+    if ((rc = plan_auto(&P[G_FC1], r->xm, C, bw.fc1_w, C, M, c.mlp_hidden, C, EPI_GELU_BF16, e)))
       return rc;
     memset(&e, 0, sizeof e);
     e.bias = bw.fc2_b;
@@ -298,8 +303,8 @@ int build_plans(ddit_req* r) {
     e.gate = mod + 5 * C;
     e.gate_stride = 6 * C;
     e.rows_per_b = rpb;
-    if ((rc = gemm_plan_init(&P[G_FC2], r->big, c.mlp_hidden, bw.fc2_w, c.mlp_hidden, M, C,
-                             c.mlp_hidden, EPI_RESID, e, bn_c)))
+    if ((rc = plan_auto(&P[G_FC2], r->big, c.mlp_hidden, bw.fc2_w, c.mlp_hidden, M, C,
+                        c.mlp_hidden, EPI_RESID, e)))
       return rc;
   }
   return DDIT_OK;
