@@ -188,6 +188,14 @@ DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int
 DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* workspace,
                                uint64_t bytes, const float* y_cond, void* stream, ddit_req** out);
 DDIT_API void ddit_request_close(ddit_req* r);
+/* Re-bind an open request (same shape / DoP / rank) to a new caption: recomputes the text
+ * embedding and the cross-attention K/V cache. Lets a serving loop keep pools of opened rank
+ * states (workspace, tables, GEMM / attention plans) instead of re-opening per request. */
+DDIT_API int ddit_request_set_text(ddit_req* r, const float* y_cond, void* stream);
+/* Promotion / re-shard broadcast (reference OverheadModel.broadcast_seconds, engine.py:52-61):
+ * copy src's text embedding and cross-attention K/V cache into dst (same model; dst may live on
+ * another peer-enabled device -- the copy then crosses NVLink). */
+DDIT_API int ddit_request_copy_text(ddit_req* dst, const ddit_req* src, void* stream);
 
 /* DoP > 1: register every rank's exchange buffers (x_sp, x_tp: fp32, as returned by
  * ddit_request_exchange_buffers on that rank, peer-mapped) and flag arrays (uint32 [P]). */

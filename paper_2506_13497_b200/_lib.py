@@ -136,6 +136,8 @@ _SIGNATURES = {
     "ddit_request_shard": [vp, ctypes.POINTER(CReqDesc)] + [ctypes.POINTER(ci)] * 4,
     "ddit_request_open": [vp, ctypes.POINTER(CReqDesc), vp, ctypes.c_uint64, vp, vp,
                           ctypes.POINTER(vp)],
+    "ddit_request_set_text": [vp, vp, vp],
+    "ddit_request_copy_text": [vp, vp, vp],
     "ddit_request_exchange_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "ddit_request_set_peers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "ddit_dit_step": [vp, vp, ci, vp],

@@ -556,6 +556,57 @@ DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int
   return DDIT_OK;
 }
 
+// Caption -> per-request text state: [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb
+// [B*300, C], then the per-block cross-attention K/V cache kv[k] = yemb . Wkv^T + b.
+static int embed_text(ddit_req* r, const float* y_cond, cudaStream_t s) {
+  const ddit_model* m = r->m;
+  const ddit_config& c = m->cfg;
+  const Geometry& g = r->g;
+  int rc;
+  // [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb [B*300, C]
+  const int Ly = g.B * c.text_tokens;
+  const size_t ycount = (size_t)c.text_tokens * c.caption_channels;
+  bf16* ycat = r->big;
+  bf16* yhid = r->big + (size_t)Ly * c.caption_channels;
+  cast_bf16(y_cond, ycat, ycount, s);
+  cast_bf16(m->w.y_null, ycat + ycount, ycount, s);
+  GemmPlan gp;
+  EpiParams e;
+  memset(&e, 0, sizeof e);
+  e.bias = m->w.y1_b;
+  e.out = yhid;
+  e.ldo = c.hidden;
+  if ((rc = gemm_plan_init(&gp, ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly,
+                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, pick_bn(c.hidden))) ||
+      (rc = launch(gp, s))) {
+    set_error("y_embedder fc1: %s", gemm_last_error());
+    return DDIT_E_CUDA;
+  }
+  e.bias = m->w.y2_b;
+  e.out = r->yemb;
+  if ((rc = gemm_plan_init(&gp, yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden,
+                           EPI_BF16, e, pick_bn(c.hidden))) ||
+      (rc = launch(gp, s))) {
+    set_error("y_embedder fc2: %s", gemm_last_error());
+    return DDIT_E_CUDA;
+  }
+  // per-block cross-attention K/V cache: kv[k] = yemb . Wkv^T + b  [B*300, 2C]
+  for (int k = 0; k < 2 * c.depth; ++k) {
+    memset(&e, 0, sizeof e);
+    e.bias = m->blocks[k].ckv_b;
+    e.out = r->kv + (size_t)k * Ly * 2 * c.hidden;
+    e.ldo = 2 * c.hidden;
+    if ((rc = gemm_plan_init(&gp, r->yemb, c.hidden, m->blocks[k].ckv_w, c.hidden, Ly,
+                             2 * c.hidden, c.hidden, EPI_BF16, e, pick_bn(2 * c.hidden))) ||
+        (rc = launch(gp, s))) {
+      set_error("cross kv: %s", gemm_last_error());
+      delete r;
+      return DDIT_E_CUDA;
+    }
+  }
+  return check_cuda("embed_text");
+}
+
 DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* workspace,
                                uint64_t bytes, const float* y_cond, void* stream, ddit_req** out) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -617,48 +668,9 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   const int base_size = (int)std::lround(std::sqrt((double)g.S));
   const float scale = (float)(std::sqrt((double)d->height * d->width) / c.input_sq_size);
   build_tables(r->pos, g.h, g.w, c.hidden, scale, (float)base_size, r->rope, g.T, c.head_dim, s);
-  // text: [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb [B*300, C]
-  const int Ly = g.B * c.text_tokens;
-  const size_t ycount = (size_t)c.text_tokens * c.caption_channels;
-  bf16* ycat = r->big;
-  bf16* yhid = r->big + (size_t)Ly * c.caption_channels;
-  cast_bf16(y_cond, ycat, ycount, s);
-  cast_bf16(m->w.y_null, ycat + ycount, ycount, s);
-  GemmPlan gp;
-  EpiParams e;
-  memset(&e, 0, sizeof e);
-  e.bias = m->w.y1_b;
-  e.out = yhid;
-  e.ldo = c.hidden;
-  if ((rc = gemm_plan_init(&gp, ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly,
-                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, pick_bn(c.hidden))) ||
-      (rc = launch(gp, s))) {
-    set_error("y_embedder fc1: %s", gemm_last_error());
+  if ((rc = embed_text(r, y_cond, s))) {
     delete r;
-    return DDIT_E_CUDA;
-  }
-  e.bias = m->w.y2_b;
-  e.out = r->yemb;
-  if ((rc = gemm_plan_init(&gp, yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden,
-                           EPI_BF16, e, pick_bn(c.hidden))) ||
-      (rc = launch(gp, s))) {
-    set_error("y_embedder fc2: %s", gemm_last_error());
-    delete r;
-    return DDIT_E_CUDA;
-  }
-  // per-block cross-attention K/V cache: kv[k] = yemb . Wkv^T + b  [B*300, 2C]
-  for (int k = 0; k < 2 * c.depth; ++k) {
-    memset(&e, 0, sizeof e);
-    e.bias = m->blocks[k].ckv_b;
-    e.out = r->kv + (size_t)k * Ly * 2 * c.hidden;
-    e.ldo = 2 * c.hidden;
-    if ((rc = gemm_plan_init(&gp, r->yemb, c.hidden, m->blocks[k].ckv_w, c.hidden, Ly,
-                             2 * c.hidden, c.hidden, EPI_BF16, e, pick_bn(2 * c.hidden))) ||
-        (rc = launch(gp, s))) {
-      set_error("cross kv: %s", gemm_last_error());
-      delete r;
-      return DDIT_E_CUDA;
-    }
+    return rc;
   }
   if ((rc = build_plans(r))) {
     set_error("plan: %s", gemm_last_error());
@@ -678,6 +690,25 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
 }
 
 DDIT_API void ddit_request_close(ddit_req* r) { delete r; }
+
+DDIT_API int ddit_request_set_text(ddit_req* r, const float* y_cond, void* stream) {
+  return embed_text(r, y_cond, static_cast<cudaStream_t>(stream));
+}
+
+DDIT_API int ddit_request_copy_text(ddit_req* dst, const ddit_req* src, void* stream) {
+  const ddit_config& c = dst->m->cfg;
+  if (src->m->cfg.hidden != c.hidden || src->m->cfg.depth != c.depth ||
+      src->m->cfg.text_tokens != c.text_tokens || src->g.B != dst->g.B) {
+    set_error("copy_text: requests of different models");
+    return DDIT_E_CONFIG;
+  }
+  const size_t Ly = (size_t)dst->g.B * c.text_tokens;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // plain UVA copies: peer-to-peer over NVLink when src lives on another (peer-enabled) device
+  cudaMemcpyAsync(dst->yemb, src->yemb, Ly * c.hidden * 2, cudaMemcpyDefault, s);
+  cudaMemcpyAsync(dst->kv, src->kv, (size_t)2 * c.depth * Ly * 2 * c.hidden * 2, cudaMemcpyDefault, s);
+  return check_cuda("ddit_request_copy_text");
+}
 
 DDIT_API int ddit_request_exchange_buffers(ddit_req* r, void** x_sp, void** x_tp, void** flags) {
   *x_sp = r->x_sp;

@@ -15,6 +15,12 @@ allocator / policy decision stays the reference's.
 * Engine GPU ids map onto physical devices ``gpu_id % device_count``. A group whose ids all
   land on one device runs as virtual ranks in lockstep (``VirtualGroup``); a group spanning
   devices runs one rank per device concurrently with the peer-store exchange.
+* Rank states (workspace, tables, GEMM / attention plans) are pooled per (resolution, devices):
+  a new request re-binds a pooled group to its caption (``ddit_request_set_text``); a promotion
+  takes a pooled group for the new GPU set and broadcasts the text state from the old rank 0
+  (``ddit_request_copy_text``) together with the latent re-shard, which is what the reference's
+  broadcast + scale-up constants stand for. ``reshard_seconds`` is that device work (CUDA events,
+  max over the new ranks when the group is emulated); ``reshard_host_seconds`` the host wall time.
 * ``profile_b200`` measures ``dit_step_seconds`` per (resolution, DoP) and emits the
   reference's ``dit-profile/1`` document (profiles.py:132-215).
 """
@@ -71,6 +77,7 @@ class _Live:
     ranks: list[StepRequest]
     shards: list[torch.Tensor]  # z T-shards, rank order
     group: VirtualGroup | None = None
+    key: tuple = ()  # pool key: (resolution, devices)
     steps_done: int = 0
     history: list[tuple[int, ...]] = field(default_factory=list)
 
@@ -107,6 +114,9 @@ class B200Executor:
         # (measured 770 GB/s peer copy), so one B200 can replay an 8-GPU trace.
         self.emulate_group = emulate_group
         self.nvlink_gbs = nvlink_gbs
+        self.pool: dict[tuple, list[_Live]] = {}  # (resolution, devices) -> idle groups
+        self.pool_limit = 4
+        self.reshard_host_seconds: list[float] = []
 
     # ---------------------------------------------------------------- helpers
     def device_of(self, gpu_id: int) -> int:
@@ -125,7 +135,26 @@ class B200Executor:
         return synthetic_inputs(self.cfg, sh.latent, seed_z=self.seed_base + 2 * request.request_id,
                                 seed_y=self.seed_base + 2 * request.request_id + 1)
 
-    def _open(self, request: RequestState, gpu_ids: tuple[int, ...]) -> _Live:
+    def _open(self, request: RequestState, gpu_ids: tuple[int, ...],
+              text_from: StepRequest | None = None) -> _Live:
+        """A group for ``gpu_ids``: pooled if one is idle (re-bound to this request's caption, or
+        given ``text_from``'s text state by a broadcast copy), else newly opened."""
+        devs = [self.device_of(g) for g in gpu_ids]
+        key = (request.resolution, tuple(devs))
+        idle = self.pool.get(key)
+        if idle:
+            live = idle.pop()
+            live.gpu_ids = tuple(gpu_ids)
+            live.steps_done, live.history = 0, []
+            if text_from is None:
+                _, y = self._inputs(request)
+                for r, d in zip(live.ranks, devs):
+                    with torch.cuda.device(d):
+                        r.set_text(y)
+            return live
+        return self._open_new(request, gpu_ids)
+
+    def _open_new(self, request: RequestState, gpu_ids: tuple[int, ...]) -> _Live:
         sh = self._shape(request)
         _, y = self._inputs(request)
         devs = [self.device_of(g) for g in gpu_ids]
@@ -157,7 +186,7 @@ class B200Executor:
             Tl = r.shard.t_hi - r.shard.t_lo
             shards.append(torch.empty((1, self.cfg.in_channels, Tl, *sh.latent[1:]),
                                       device=torch.device("cuda", d)))
-        return _Live(tuple(gpu_ids), ranks, shards, group)
+        return _Live(tuple(gpu_ids), ranks, shards, group, key=(request.resolution, tuple(devs)))
 
     # ---------------------------------------------------------------- StepExecutor protocol
     def dit_step(self, request: RequestState, gpu_ids: tuple[int, ...], step: int,
@@ -171,14 +200,25 @@ class B200Executor:
                 zs.copy_(z0[:, :, r.shard.t_lo:r.shard.t_hi])
             self.live[request.request_id] = live
         elif tuple(gpu_ids) != live.gpu_ids:  # promotion P -> P': re-shard at the boundary
-            new = self._open(request, gpu_ids)
+            new = self._open(request, gpu_ids, text_from=live.ranks[0])
             srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
+            spans = []
             for r, zs in zip(new.ranks, new.shards):
                 with torch.cuda.device(zs.device):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
                     latent_gather(zs, r.shard.t_lo, r.shard.t_hi, srcs)
+                    r.copy_text_from(live.ranks[0])
+                    b.record()
+                    spans.append((a, b))
             for d in {zs.device.index for zs in new.shards}:
                 torch.cuda.synchronize(d)
-            self.reshard_seconds.append(time.perf_counter() - t0)
+            per = [a.elapsed_time(b) / 1e3 for a, b in spans]
+            one_device = len({zs.device.index for zs in new.shards}) == 1
+            # ranks on P GPUs re-shard concurrently; virtual ranks on one device ran one by one
+            dev_s = max(per) if (self.emulate_group or not one_device) else sum(per)
+            self.reshard_seconds.append(dev_s)
+            self.reshard_host_seconds.append(time.perf_counter() - t0)
             new.steps_done = live.steps_done
             new.history = live.history + [live.gpu_ids]
             self._close(live)
@@ -204,13 +244,15 @@ class B200Executor:
         live = self.live.pop(request.request_id)
         sh = self._shape(request)
         master = self.device_of(vae_gpu_ids[0])
-        t0 = time.perf_counter()
         with torch.cuda.device(master):
             z = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
             srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
-            latent_gather(z, 0, sh.T, srcs)
-            torch.cuda.synchronize(master)
-        handoff = time.perf_counter() - t0
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            latent_gather(z, 0, sh.T, srcs)  # peer loads of every T-shard into the master
+            b.record()
+            b.synchronize()
+        handoff = a.elapsed_time(b) / 1e3
         self.final_latents[request.request_id] = z
         self._close(live)
         decode = 0.0
@@ -259,8 +301,20 @@ class B200Executor:
         return max(s.elapsed_time(e) for s, e in evs) / 1e3
 
     def _close(self, live: _Live) -> None:
+        """Return the group's rank states to the pool (closed when the pool is full)."""
+        idle = self.pool.setdefault(live.key, [])
+        if len(idle) < self.pool_limit:
+            idle.append(live)
+            return
         for r in live.ranks:
             r.close()
+
+    def close(self) -> None:
+        for idle in self.pool.values():
+            for live in idle:
+                for r in live.ranks:
+                    r.close()
+        self.pool.clear()
 
 
 def profile_b200(cfg: STDiTConfig, weights: dict[str, torch.Tensor], labels: list[str],

@@ -180,6 +180,17 @@ class StepRequest:
     def end(self, z_local, step, stream=None):
         check(lib().ddit_step_end(self.handle, z_local.data_ptr(), step, stream_ptr(stream)))
 
+    def set_text(self, y_cond: torch.Tensor, stream=None) -> None:
+        """Re-bind this (pooled) rank state to a new caption [1|., 300, 4096]."""
+        y = y_cond.to(self.model.device, torch.float32).reshape(self.model.cfg.text_tokens, -1).contiguous()
+        self._y = y
+        check(lib().ddit_request_set_text(self.handle, y.data_ptr(), stream_ptr(stream)))
+
+    def copy_text_from(self, src: "StepRequest", stream=None) -> None:
+        """Broadcast src's text embedding + cross-attention K/V cache into this rank (a peer copy
+        when src lives on another GPU) -- the promotion-time state transfer."""
+        check(lib().ddit_request_copy_text(self.handle, src.handle, stream_ptr(stream)))
+
     def exchange_buffers(self) -> tuple[int, int, int]:
         a, b, c = vp(), vp(), vp()
         check(lib().ddit_request_exchange_buffers(self.handle, ctypes.byref(a), ctypes.byref(b),

@@ -118,9 +118,12 @@ def main() -> None:
             **metrics_of(res), "steps_executed": steps, "vae_decodes": len(rex.vae_seconds),
             "reshards": len(rex.reshard_seconds),
             "reshard_ms_max": round(1e3 * max(rex.reshard_seconds), 3) if rex.reshard_seconds else None,
+            "reshard_host_ms_max": (round(1e3 * max(rex.reshard_host_seconds), 3)
+                                    if rex.reshard_host_seconds else None),
             "handoff_ms_max": round(1e3 * max(h for _, h, _ in rex.vae_seconds), 3),
             "wall_seconds": round(time.time() - t1, 1)}
         print("replayed", r, out["replayed"][f"{r:g}"], flush=True)
+        rex.close()
         for m in rex.models.values():
             m.close()
         del rex
