@@ -41,6 +41,11 @@ DDIT_API int ddit_num_sms(void);
 /* GEMM kernel selection for plans built afterwards: 1 (default) = cta_group::2 kernel
  * (256-row tiles over a CTA pair), 0 = single-CTA kernel (128-row tiles). Env DDIT_GEMM_2CTA=0. */
 DDIT_API int ddit_set_gemm_2cta(int on);
+/* DoP > 1: fuse the DSP exchange into every block's fc2 GEMM -- the gated-residual epilogue
+ * stores each updated row straight into its owner rank's buffer of the other layout (peer
+ * memory over NVLink) and the kernel's last CTA publishes the exchange flag; 0 = the separate
+ * exchange kernel. Default 1 (env DDIT_FUSED_XCH=0); applies to peers registered afterwards. */
+DDIT_API int ddit_set_fused_exchange(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */

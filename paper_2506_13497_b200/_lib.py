@@ -127,6 +127,7 @@ class Attn(ctypes.Structure):
 _SIGNATURES = {
     "ddit_set_gemm_2cta": [ci],
     "ddit_set_pdl": [ci],
+    "ddit_set_fused_exchange": [ci],
     "ddit_enable_peer_access": [ci, ci],
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],

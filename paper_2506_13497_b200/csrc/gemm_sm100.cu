@@ -253,6 +253,37 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
 }
 
 // ------------------------------------------------------------------ epilogue: gated residual
+// Destination of row `row` (of this rank's layout) in its owner rank's other-layout buffer.
+DDIT_DEV float* xch_row(const EpiParams& ep, int row, int C) {
+  if (ep.xch == 1) {  // x_sp [B][Tl][S] -> x_tp of rank q [B][T][Sl_q]
+    const int s = row % ep.xS, tl = (row / ep.xS) % ep.xlen, b = row / (ep.xS * ep.xlen);
+    const int q = s / ep.xchunk, s_lo = q * ep.xchunk;
+    const int Sl = min(s_lo + ep.xchunk, ep.xS) - s_lo;
+    return ep.xdst[q] + (((size_t)b * ep.xT + ep.xlo + tl) * Sl + (s - s_lo)) * C;
+  }
+  // x_tp [B][T][Sl] -> x_sp of rank q [B][Tl_q][S]
+  const int sl = row % ep.xlen, t = (row / ep.xlen) % ep.xT, b = row / (ep.xlen * ep.xT);
+  const int q = t / ep.xchunk, t_lo = q * ep.xchunk;
+  const int Tlq = min(t_lo + ep.xchunk, ep.xT) - t_lo;
+  return ep.xdst[q] + (((size_t)b * Tlq + (t - t_lo)) * ep.xS + ep.xlo + sl) * C;
+}
+
+// End of a fused-exchange GEMM: after every CTA's stores, the last CTA (ticket) publishes the
+// new epoch into every rank's flag slot for this rank (same protocol as exchange.cu).
+DDIT_DEV void xch_signal(const EpiParams& ep) {
+  if (threadIdx.x != 0 || ep.xflags[0] == nullptr) return;
+  __threadfence_system();
+  const unsigned int ticket = atomicAdd(ep.xcounter, 1u);
+  if (ticket != gridDim.x - 1) return;
+  *ep.xcounter = 0;
+  __threadfence_system();
+  const uint32_t e = *ep.xepoch + 1;
+  *ep.xepoch = e;
+  for (int q = 0; q < ep.xP; ++q)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(ep.xflags[q] + ep.xrank), "r"(e)
+                 : "memory");
+}
+
 // x[r, c] += gate[b(r), c] * (acc + bias[c]) in fp32 through TMA (load, update in smem, store),
 // plus an optional bf16 copy of the new x (the cross-attention query input).
 // Every epilogue warp owns the 32 accumulator rows of its TMEM lane quarter and runs an
@@ -273,6 +304,15 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
   const int row = m0 + ew * 32 + lane;
   const int grow = row < cx.M ? row : cx.M - 1;
   const float* gate_row = ep.gate ? ep.gate + (size_t)(grow / ep.rows_per_b) * ep.gate_stride : nullptr;
+  // fused exchange: lane l copies rows 4i + l/8 (i < 8), 16 B chunk l%8 of each sub-tile row
+  float* xrow[8];
+  if (ep.xch) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gr = m0 + ew * 32 + 4 * i + (lane >> 3);
+      xrow[i] = gr < cx.M ? xch_row(ep, gr, ep.ldr) : nullptr;
+    }
+  }
 #pragma unroll 1
   for (int sub = 0; sub < NS; ++sub) {
     const int slot = cnt % R;
@@ -326,12 +366,25 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
                      pack_bf16(nv[8 * j + 2], nv[8 * j + 3]), pack_bf16(nv[8 * j + 4], nv[8 * j + 5]),
                      pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
     }
-    fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(tmR, rb, col0, m0 + ew * 32);
-      if (ep.out2) tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
-      bulk_commit();
+    if (ep.xch) {  // rows go to their owner rank (peer stores), 4 whole 128 B rows per instruction
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (xrow[i] != nullptr) {
+          const float4 v = ld_shared_f4(rbase + sw128(4 * i + (lane >> 3), lane & 7));
+          *reinterpret_cast<float4*>(xrow[i] + col0 + 4 * (lane & 7)) = v;
+        }
+      }
+      fence_async_smem();  // generic reads of the slot before its next TMA load
+      __syncwarp();
+    } else {
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmR, rb, col0, m0 + ew * 32);
+        if (ep.out2) tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
+        bulk_commit();
+      }
     }
     ++cnt;
   }
@@ -572,6 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (EPI == EPI_RESID) {
+    if (ep.xch) xch_signal(ep);
+  }
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
@@ -789,6 +845,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  if constexpr (EPI == EPI_RESID) {
+    if (ep.xch) xch_signal(ep);
+  }
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),

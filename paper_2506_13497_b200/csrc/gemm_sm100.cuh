@@ -37,6 +37,17 @@ struct EpiParams {
   int rope_S;               // tokens per frame in this row layout: t = (row / rope_S) % rope_T
   const float2* rope_tab;   // [rope_T][head_dim/2] (cos, sin)
   float eps;
+  // EPI_RESID with the DSP exchange fused in (xch != 0): the updated rows are stored straight
+  // into their owner rank's buffer of the other layout (peer memory) instead of back into
+  // resid, and the last CTA publishes the exchange flag (layouts: exchange.cu)
+  int xch;                  // 0: none, 1: x_sp -> x_tp (spatial block), 2: x_tp -> x_sp (temporal)
+  float* xdst[8];           // destination buffer of every rank
+  int xB, xT, xS, xP;       // CFG batch, frames, tokens per frame, DoP
+  int xlo, xlen, xchunk;    // 1: t_lo, Tl, ceil(S/P); 2: s_lo, Sl, ceil(T/P)
+  uint32_t* xflags[8];      // every rank's flag array; all null: ranks ordered by the stream
+  unsigned int* xcounter;   // CTA ticket counter (zero between exchanges)
+  uint32_t* xepoch;         // this rank's exchange epoch
+  int xrank;
 };
 
 struct GemmPlan {

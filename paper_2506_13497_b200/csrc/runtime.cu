@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <atomic>
 #include <new>
 #include <vector>
@@ -152,6 +153,7 @@ struct ddit_req {
   bool peers_set = false;
   bool flags_set = false;
   bool use_tc_attention = true;  // tcgen05 FMHA for spatial / cross attention
+  bool fused_xch = false;        // the fc2 GEMM of every block performs the DSP exchange
   // profiling: event pairs around every launch, tagged by kernel class
   bool prof_on = false;
   std::vector<cudaEvent_t> ev;
@@ -163,6 +165,17 @@ struct ddit_req {
 };
 
 static std::atomic<unsigned long long> g_launches{0};
+
+// GEMM -> exchange fusion for DoP > 1 (env DDIT_FUSED_XCH=0 / ddit_set_fused_exchange(0): the
+// separate exchange kernel), read when a request's peers are registered
+static int g_fused_xch = -1;
+static bool fused_exchange_enabled() {
+  if (g_fused_xch < 0) {
+    const char* e = getenv("DDIT_FUSED_XCH");
+    g_fused_xch = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_fused_xch != 0;
+}
 
 namespace {
 enum { K_GEMM = 0, K_ATTN = 1, K_EW = 2, K_EXCH = 3, K_NCLASS = 4 };
@@ -468,6 +481,9 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
 int push_exchange(ddit_req* r, int k, cudaStream_t s) {
   const Geometry& g = r->g;
   if (g.P == 1) return DDIT_OK;
+  // fused: the block's fc2 GEMM already stored its rows at their owners and signalled (a rank
+  // without rows in this layout runs no GEMM, so it still signals through the exchange kernel)
+  if (r->fused_xch && ((k & 1) ? g.M_tp : g.M_sp) > 0) return DDIT_OK;
   if (!r->peers_set) {
     set_error("DoP %d request has no peers registered", g.P);
     return DDIT_E_CONFIG;
@@ -726,6 +742,30 @@ DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const*
   }
   r->peers_set = true;
   r->flags_set = flags != nullptr;
+  // GEMM -> exchange fusion: every block's fc2 plan stores its rows at their owner rank
+  const Geometry& g = r->g;
+  r->fused_xch = g.P > 1 && fused_exchange_enabled();
+  for (int k = 0; k < 2 * r->m->cfg.depth && !r->plans.empty(); ++k) {
+    EpiParams& e = r->plans[(size_t)k * G_N + G_FC2].ep;
+    e.xch = 0;
+    if (!r->fused_xch) continue;
+    const bool temporal = k & 1;
+    e.xch = temporal ? 2 : 1;
+    for (int q = 0; q < kMaxDop; ++q) {
+      e.xdst[q] = q < g.P ? (temporal ? r->peer_sp.p[q] : r->peer_tp.p[q]) : nullptr;
+      e.xflags[q] = q < g.P && r->flags_set ? r->peer_flags.p[q] : nullptr;
+    }
+    e.xB = g.B;
+    e.xT = g.T;
+    e.xS = g.S;
+    e.xP = g.P;
+    e.xlo = temporal ? g.s_lo : g.t_lo;
+    e.xlen = temporal ? g.Sl : g.Tl;
+    e.xchunk = temporal ? (g.T + g.P - 1) / g.P : (g.S + g.P - 1) / g.P;
+    e.xcounter = r->counter;
+    e.xepoch = r->counter + 1;
+    e.xrank = g.rank;
+  }
   return DDIT_OK;
 }
 
@@ -788,6 +828,11 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->counter + 1, r->g.P, s); });
   return check_cuda("barrier");
+}
+
+DDIT_API int ddit_set_fused_exchange(int on) {
+  g_fused_xch = on ? 1 : 0;
+  return DDIT_OK;
 }
 
 DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value) {

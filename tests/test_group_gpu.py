@@ -10,12 +10,15 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["fused-xch", "xch-kernel"])
 @pytest.mark.parametrize("dop", [2, 4])
-def test_multiprocess_group_matches_dop1(cuda, dop):
-    port = 29600 + dop
+def test_multiprocess_group_matches_dop1(cuda, dop, fused):
+    """Real processes with CUDA-IPC peer buffers and the flag barrier; the exchange fused into
+    the fc2 GEMM (DDIT_FUSED_XCH=1) or as the separate kernel."""
+    port = 29600 + 2 * dop + int(fused)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={dop}",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "scripts" / "group_check.py"), "144p"]
-    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env = dict(os.environ, OMP_NUM_THREADS="1", DDIT_FUSED_XCH=fused)
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240, env=env, cwd=ROOT)
     print(res.stdout[-3000:], res.stderr[-3000:])
     assert res.returncode == 0

@@ -70,19 +70,27 @@ def test_xl2_width_step_matches_oracle(cuda, label):
     assert e_z <= 1e-2 and e_v <= 2e-2
 
 
+@pytest.mark.parametrize("fused", [1, 0], ids=["fused-xch", "xch-kernel"])
+@pytest.mark.parametrize("label", ["144p", "240p"])
 @pytest.mark.parametrize("dop", [2, 4, 8])
-def test_virtual_dop_matches_dop1(cuda, dop):
-    """DoP-P shards + exchange (virtual ranks on one device) reproduce the DoP-1 step."""
-    from paper_2506_13497_b200 import weights
+def test_virtual_dop_matches_dop1(cuda, dop, label, fused):
+    """DoP-P shards + exchange (virtual ranks on one device) reproduce the DoP-1 step, with the
+    exchange fused into the fc2 GEMM epilogue (peer stores) or as the separate kernel.
+    144p: T=15 (ragged T shards), S=144; 240p: S=405 (ragged S shards at every P)."""
+    from paper_2506_13497_b200 import _lib, weights
     from paper_2506_13497_b200.stdit import STDiTModel, StepRequest, VirtualGroup
 
     cfg = dataclasses.replace(weights.TINY, depth=2)
-    W, sh, z, y = _setup(cfg, "144p")  # T=15, S=144: ragged T shards at every P
+    W, sh, z, y = _setup(cfg, label)
     model = STDiTModel(cfg, W, cuda)
     yd = y.to(cuda)
     z1 = z.to(cuda).contiguous()
     StepRequest(model, sh, yd).step(z1, 5)
-    grp = VirtualGroup(model, sh, yd, dop)
+    _lib.lib().ddit_set_fused_exchange(fused)
+    try:
+        grp = VirtualGroup(model, sh, yd, dop)
+    finally:
+        _lib.lib().ddit_set_fused_exchange(1)
     parts = grp.split(z.to(cuda))
     grp.step(parts, 5)
     zp = torch.cat(parts, dim=2)
