@@ -3,54 +3,67 @@
 // all blocks, patch-embed + pos-embed (step entry), and the fused exit (final LayerNorm +
 // modulate + Linear + unpatchify + CFG combine + rectified-flow Euler update).
 #include "common.cuh"
+#include <cstdlib>
 #include "elementwise.cuh"
 
 namespace ddit {
 
 // ------------------------------------------------------------------ LN + modulate (K1)
 // xm[r, :] = bf16( LN(x[r, :]) * (1 + scale[b]) + shift[b] ),  b = r / rows_per_b.
-// One warp per row; C % 4 == 0 and C <= 32 * 4 * kMaxVec.
-static constexpr int kMaxVec = 12;  // C up to 1536
+// LPR lanes per row, NV float4 per lane (the whole row in registers, C = 4 * LPR * NV exactly
+// for the instantiated widths, else the generic NV = kMaxVec path with bounds checks): two-pass
+// statistics from registers, x streamed once (__ldcs), shift / scale through L1.
+static constexpr int kMaxVec = 12;  // generic path: C up to 1536 with 32 lanes
 
-__global__ void __launch_bounds__(256)
+template <int LPR>
+DDIT_DEV float group_sum(float v) {
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NV, int LPR, bool EXACT>
+__global__ void __launch_bounds__(128)
     ln_modulate_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int M, int C,
                        const float* __restrict__ shift, const float* __restrict__ scale,
                        int mod_stride, int rows_per_b, float eps) {
   pdl_wait();
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * C);
+  constexpr int RPB = 128 / LPR;  // rows per block
+  const int row = blockIdx.x * RPB + (threadIdx.x / LPR);
+  const int lane = threadIdx.x % LPR;
+  const bool live = row < M;  // all lanes of a warp take part in the shuffles
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)(live ? row : 0) * C);
   const int nv = C >> 2;
-  float4 v[kMaxVec];
+  float4 v[NV];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < kMaxVec; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nv) {
-      v[i] = __ldg(xr + c);
-      s += v[i].x + v[i].y + v[i].z + v[i].w;
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + LPR * i;
+    if (live && (EXACT || c < nv)) {
+      v[i] = __ldcs(xr + c);
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     }
   }
-  const float mean = warp_sum(s) / C;
+  const float mean = group_sum<LPR>(s) / C;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < kMaxVec; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nv) {
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + LPR * i;
+    if (live && (EXACT || c < nv)) {
       const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
-      q += a * a + b * b + cc * cc + d * d;
+      q += (a * a + b * b) + (cc * cc + d * d);
     }
   }
-  const float rstd = rsqrtf(warp_sum(q) / C + eps);
+  const float rstd = rsqrtf(group_sum<LPR>(q) / C + eps);
+  if (!live) return;
   const int bidx = row / rows_per_b;
   const float4* sh = reinterpret_cast<const float4*>(shift + (size_t)bidx * mod_stride);
   const float4* sc = reinterpret_cast<const float4*>(scale + (size_t)bidx * mod_stride);
   uint2* o = reinterpret_cast<uint2*>(out + (size_t)row * C);
 #pragma unroll
-  for (int i = 0; i < kMaxVec; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nv) {
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + LPR * i;
+    if (EXACT || c < nv) {
       const float4 a = __ldg(sh + c), k = __ldg(sc + c);
       const float y0 = (v[i].x - mean) * rstd * (1.f + k.x) + a.x;
       const float y1 = (v[i].y - mean) * rstd * (1.f + k.y) + a.y;
@@ -61,11 +74,26 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+static int g_ln_variant = -1;  // tuning hook (env DDIT_LN): 0 generic, 1 = 32 lanes x 9, 2 = 16 x 18
+
 int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
                 const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s) {
   if (C % 4 || C > 32 * 4 * kMaxVec || M <= 0) return -2;
-  launch_pdl(ln_modulate_kernel, dim3((M + 7) / 8), dim3(256), 0, s, x, out, M, C, shift, scale,
-             mod_stride, rows_per_b > 0 ? rows_per_b : M, eps);
+  if (g_ln_variant < 0) {
+    const char* e = getenv("DDIT_LN");
+    g_ln_variant = e ? atoi(e) : 1;
+  }
+  const int rpb = rows_per_b > 0 ? rows_per_b : M;
+  if (C == 1152 && g_ln_variant == 1) {
+    launch_pdl(ln_modulate_kernel<9, 32, true>, dim3((M + 3) / 4), dim3(128), 0, s, x, out, M, C,
+               shift, scale, mod_stride, rpb, eps);
+  } else if (C == 1152 && g_ln_variant == 2) {
+    launch_pdl(ln_modulate_kernel<18, 16, true>, dim3((M + 7) / 8), dim3(128), 0, s, x, out, M, C,
+               shift, scale, mod_stride, rpb, eps);
+  } else {
+    launch_pdl(ln_modulate_kernel<kMaxVec, 32, false>, dim3((M + 3) / 4), dim3(128), 0, s, x, out,
+               M, C, shift, scale, mod_stride, rpb, eps);
+  }
   return 0;
 }
 
