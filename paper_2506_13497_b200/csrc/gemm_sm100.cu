@@ -28,6 +28,8 @@ static constexpr int kThreads = 256;
 static constexpr int kTmemCols = 512;
 static constexpr int kAccStride = 256;  // TMEM column offset of accumulator buffer 1
 
+__host__ __device__ constexpr bool is_resid(int epi) { return epi == EPI_RESID || epi == EPI_RESID_COPY; }
+
 template <int BN, int EPI>
 struct EpiCfg {
   // staging bytes (two buffers) and sub-tile width (columns) per epilogue kind: bf16 outputs
@@ -37,13 +39,16 @@ struct EpiCfg {
   static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
   // gated residual: each epilogue warp runs its own ring of RSLOTS fp32 32x32 sub-tiles (loads run
   // RSLOTS-2 sub-tiles ahead) + three bf16 copy buffers (SW64): WARP_BYTES per warp
-  static constexpr int RSLOTS = EPI == EPI_RESID ? 2 : 0;
+  static constexpr int RSLOTS = is_resid(EPI) ? 2 : 0;
   // R >= 3: stores of sub-tile s-1 may still read while s runs (3 bf16 buffers, loads R-2 ahead);
   // R == 2: they must finish first (2 bf16 buffers, loads 1 ahead)
   static constexpr int RAHEAD = RSLOTS >= 3 ? RSLOTS - 2 : 1;
   static constexpr int NOB = RSLOTS >= 3 ? 3 : 2;
-  static constexpr int WARP_BYTES = RSLOTS * 4096 + NOB * 2048;
-  static constexpr int BYTES = EPI == EPI_RESID ? 4 * WARP_BYTES : 2 * BUF;
+  // EPI_RESID_COPY: the bf16 copy of a PAIR of sub-tiles (32 rows x 64 cols, 128 B rows) leaves
+  // in one TMA store -- 64 B-row boxes store at a fraction of the bandwidth
+  static constexpr int OB = EPI == EPI_RESID_COPY ? 4096 : 2048;
+  static constexpr int WARP_BYTES = RSLOTS * 4096 + NOB * OB;
+  static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES : 2 * BUF;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
 
@@ -291,14 +296,17 @@ DDIT_DEV void xch_signal(const EpiParams& ep) {
 // RSLOTS-deep ring whose loads run RSLOTS-2 sub-tiles ahead (across tile boundaries), its own
 // TMA stores leave from the same slot, and no CTA-wide barrier is involved -- the four warps
 // drift freely, so one warp's HBM latency hides behind the others' math.
-template <int BN>
+template <int BN, int EPI>
 DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const CUtensorMap* tmO2,
                              uint8_t* sE, uint64_t* rbar, uint32_t taddr, int ew, int lane,
                              int m0, int n0, const EpiCtx& cx, const ResidStream& rs,
                              int& cnt, uint32_t tempty_cl) {
   constexpr int NS = BN / 32;
-  constexpr int R = EpiCfg<BN, EPI_RESID>::RSLOTS;
-  uint8_t* wbase = sE + ew * EpiCfg<BN, EPI_RESID>::WARP_BYTES;
+  constexpr bool COPY = EPI == EPI_RESID_COPY;
+  static_assert(!COPY || NS % 2 == 0, "paired bf16 copy needs BN % 64 == 0");
+  using Cfg = EpiCfg<BN, EPI>;
+  constexpr int R = Cfg::RSLOTS;
+  uint8_t* wbase = sE + ew * Cfg::WARP_BYTES;
   uint64_t* wbar = rbar + ew * R;
   const int rit = lane;  // row within the warp's slab (swizzle phase = lane & 7)
   const int row = m0 + ew * 32 + lane;
@@ -317,7 +325,9 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
   for (int sub = 0; sub < NS; ++sub) {
     const int slot = cnt % R;
     uint8_t* rb = wbase + slot * 4096;
-    uint8_t* ob = wbase + R * 4096 + (cnt % EpiCfg<BN, EPI_RESID>::NOB) * 2048;
+    // bf16 copy buffer: per sub-tile (RESID) or per sub-tile pair (COPY; pairs never straddle a
+    // tile because NS is even and cnt counts sub-tiles from 0)
+    uint8_t* ob = wbase + R * 4096 + ((COPY ? cnt >> 1 : cnt) % Cfg::NOB) * Cfg::OB;
     const int col0 = n0 + sub * 32;
     // column vectors first: their L2 latency overlaps the waits below
     float4 bv[8], gv[8];
@@ -331,8 +341,8 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
     if (lane == 0) {
       // this warp's stores up to sub-tile cnt-1-(NOB-2) have read their smem, so the ring slot
       // of sub-tile cnt+RAHEAD and the next bf16 buffer are free again
-      constexpr int AH = EpiCfg<BN, EPI_RESID>::RAHEAD;
-      bulk_wait_read<EpiCfg<BN, EPI_RESID>::NOB - 2>();
+      constexpr int AH = Cfg::RAHEAD;
+      bulk_wait_read<Cfg::NOB - 2>();
       resid_issue<R>(rs, NS, cnt + AH, ew * 32, tmR, wbase, wbar);
     }
     mbar_wait(&wbar[slot], (cnt / R) & 1);
@@ -358,7 +368,15 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
       st_shared_v4(a, __float_as_uint(nv[4 * j]), __float_as_uint(nv[4 * j + 1]),
                    __float_as_uint(nv[4 * j + 2]), __float_as_uint(nv[4 * j + 3]));
     }
-    if (ep.out2) {
+    if (COPY) {  // chunks 4h..4h+3 of the pair's 128 B row, h = sub-tile parity
+      const uint32_t obase = smem_u32(ob);
+      const int h = cnt & 1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st_shared_v4(obase + sw128(rit, 4 * h + j), pack_bf16(nv[8 * j], nv[8 * j + 1]),
+                     pack_bf16(nv[8 * j + 2], nv[8 * j + 3]), pack_bf16(nv[8 * j + 4], nv[8 * j + 5]),
+                     pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
+    } else if (ep.out2) {
       const uint32_t obase = smem_u32(ob);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -382,7 +400,11 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
       __syncwarp();
       if (lane == 0) {
         tma_store_2d(tmR, rb, col0, m0 + ew * 32);
-        if (ep.out2) tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
+        if (COPY) {
+          if (cnt & 1) tma_store_2d(tmO2, ob, col0 - 32, m0 + ew * 32);
+        } else if (ep.out2) {
+          tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
+        }
         bulk_commit();
       }
     }
@@ -507,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmO);
-    if constexpr (EPI == EPI_RESID) tma_prefetch_desc(&tmR);
+    if constexpr (is_resid(EPI)) tma_prefetch_desc(&tmR);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -589,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int cnt = 0;
     const ResidStream rs{(int)blockIdx.x, (int)gridDim.x, num_tiles, n_tiles, BM, 0};
-    if constexpr (EPI == EPI_RESID) {
+    if constexpr (is_resid(EPI)) {
       constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
       if (elected) {  // residual tiles 0 and 1 into L2
         resid_prefetch_l2<BN>(rs, 0, &tmO);
@@ -603,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m0 = (tile / n_tiles) * BM;
       const int n0 = (tile % n_tiles) * BN;
-      if constexpr (EPI == EPI_RESID) {  // two tiles ahead: lands in L2 well before its epilogue
+      if constexpr (is_resid(EPI)) {  // two tiles ahead: lands in L2 well before its epilogue
         if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
         ++tix;
       }
@@ -613,19 +635,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
-      } else if constexpr (EPI == EPI_RESID) {
-        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
+      } else if constexpr (is_resid(EPI)) {
+        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected || (EPI == EPI_RESID && lane == 0)) bulk_wait<0>();
+    if (elected || (is_resid(EPI) && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (EPI == EPI_RESID) {
+  if constexpr (is_resid(EPI)) {
     if (ep.xch) xch_signal(ep);
   }
   if (warp == 2) {
@@ -719,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmO);
-    if constexpr (EPI == EPI_RESID) tma_prefetch_desc(&tmR);
+    if constexpr (is_resid(EPI)) tma_prefetch_desc(&tmR);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -809,7 +831,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int cnt = 0;
     const ResidStream rs{cid, nclusters, num_tiles, n_tiles, BM2, (int)rank * BM};
-    if constexpr (EPI == EPI_RESID) {
+    if constexpr (is_resid(EPI)) {
       constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
       if (elected) {  // residual tiles 0 and 1 into L2
         resid_prefetch_l2<BN>(rs, 0, &tmO);
@@ -823,7 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int tile = cid; tile < num_tiles; tile += nclusters) {
       const int m0 = (tile / n_tiles) * BM2 + rank * BM;
       const int n0 = (tile % n_tiles) * BN;
-      if constexpr (EPI == EPI_RESID) {  // two tiles ahead: lands in L2 well before its epilogue
+      if constexpr (is_resid(EPI)) {  // two tiles ahead: lands in L2 well before its epilogue
         if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
         ++tix;
       }
@@ -833,19 +855,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
-      } else if constexpr (EPI == EPI_RESID) {
-        epi_resid_tile<BN>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
+      } else if constexpr (is_resid(EPI)) {
+        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected || (EPI == EPI_RESID && lane == 0)) bulk_wait<0>();
+    if (elected || (is_resid(EPI) && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   cluster_sync_all();
-  if constexpr (EPI == EPI_RESID) {
+  if constexpr (is_resid(EPI)) {
     if (ep.xch) xch_signal(ep);
   }
   if (warp == 2) {
@@ -918,6 +940,7 @@ int num_sms() {
 
 static bool bn_ok(int bn, int epi) {
   if (epi == EPI_QKV) return bn == 144;
+  if (epi == EPI_RESID_COPY) return bn == 128 || bn == 192 || bn == 256;
   if (bn == 0) return false;
   return bn == 96 || bn == 128 || bn == 192 || bn == 256;
 }
@@ -999,11 +1022,20 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
         return -3;
       break;
     case EPI_RESID:
+    case EPI_RESID_COPY:
+      // with a bf16 copy and BN % 64 == 0, the copy leaves in 64-column boxes (EPI_RESID_COPY)
+      if (ep.out2 && bn % 64 == 0) epi = EPI_RESID_COPY;
+      if (epi == EPI_RESID_COPY && (!ep.out2 || bn % 64)) {
+        snprintf(g_err, sizeof g_err, "EPI_RESID_COPY needs out2 and BN %% 64 == 0");
+        return -2;
+      }
       if (!ep.resid ||
           make_tmap(&p->tmR, ep.resid, F32, 4, M, N, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return -3;
-      if (ep.out2 &&
-          make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      if (epi == EPI_RESID_COPY
+              ? make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B)
+              : ep.out2 && make_tmap(&p->tmO2, ep.out2, BF, 2, M, N, ep.ldo2, 32, 32,
+                                     CU_TENSOR_MAP_SWIZZLE_64B))
         return -3;
       // tmO (unused by this epilogue) carries the whole-tile map for the L2 prefetch
       if (make_tmap(&p->tmO, ep.resid, F32, 4, M, N, ep.ldr, BM, bn, CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -1123,6 +1155,13 @@ int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
         case 128: return launch_t<128, EPI_RESID>(p, s);
         case 192: return launch_t<192, EPI_RESID>(p, s);
         case 256: return launch_t<256, EPI_RESID>(p, s);
+      }
+      break;
+    case EPI_RESID_COPY:
+      switch (p->bn) {
+        case 128: return launch_t<128, EPI_RESID_COPY>(p, s);
+        case 192: return launch_t<192, EPI_RESID_COPY>(p, s);
+        case 256: return launch_t<256, EPI_RESID_COPY>(p, s);
       }
       break;
     case EPI_F32:

@@ -15,6 +15,7 @@ enum EpiKind : int {
   EPI_RESID = 2,      // resid_f32 += gate[b] * (acc + bias)   (gate == null -> 1); optional bf16 copy
   EPI_QKV = 3,        // out_bf16 = rope(rmsnorm_head(acc + bias)) on the q/k sections; v: acc + bias
   EPI_F32 = 4,        // out_f32 = acc + bias
+  EPI_RESID_COPY = 5, // internal: EPI_RESID with the bf16 copy, stored in 64-column (128 B) boxes
 };
 
 struct EpiParams {
