@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         const int qi = g * 2 + (qc & 1);
         const uint32_t qa = smem_u32(sm + OFF_Q + qi * QT);
         mbar_wait(&q_full[qi], (qc >> 1) & 1);
-        if (un > 0) mbar_wait(&o_free[g], (un - 1) & 1);  // the group read its previous O
         for (int j = 0; j <= nk; ++j) {
           if (j < nk) {  // S = Q K_j^T once the group holds its previous S in registers
             mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
@@ -351,6 +350,9 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             ++kc;
           }
           if (j > 0) {  // O (+)= P_{j-1} V_{j-1} once the group wrote P
+            // the unit's first PV overwrites O: the group must have read its previous O. Only
+            // here -- the unit's first QK already ran during that epilogue
+            if (j == 1 && un > 0) mbar_wait(&o_free[g], (un - 1) & 1);
             mbar_wait(&v_full[vc % VST], (vc / VST) & 1);
             mbar_wait(&p_full[g], pn & 1);
             tc_fence_after();
