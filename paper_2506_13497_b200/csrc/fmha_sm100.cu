@@ -416,10 +416,14 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 128; e += 2)
             mx8[(e >> 1) & 7] = fmax3(mx8[(e >> 1) & 7], __uint_as_float(s[e]), __uint_as_float(s[e + 1]));
-        } else {
+        } else {  // ragged last tile: whole 8-key chunks below `valid`, then the partial one
 #pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e < valid) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(s[e]));
+          for (int c = 0; c < 16; ++c) {
+            if (c * 8 >= valid) break;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (c * 8 + e < valid) mx8[e] = fmaxf(mx8[e], __uint_as_float(s[c * 8 + e]));
+          }
         }
         const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -459,18 +463,23 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
-        } else {
+        } else {  // chunks past `valid` only get zero P (the tensor core still reads them)
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            float pv[8];
+            if (c * 8 < valid) {
+              float pv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int key = c * 8 + e;
-              pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
-              rs8[e] += pv[e];
+              for (int e = 0; e < 8; ++e) {
+                const int key = c * 8 + e;
+                pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
+                rs8[e] += pv[e];
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) s[4 * c + e] = 0u;
             }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
         }
         if (j > 0) {
