@@ -336,11 +336,14 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             tc_fence_after();
             if (elect_one()) {
               const uint32_t ka = smem_u32(sm + OFF_K + (kc % KST) * (KA + KB)), kb = ka + KA;
+              // ragged last tile: only round16(valid) key columns (the rest of S is never read)
+              const int kv16 = (min(BKV, p.Lk - j * BKV) + 15) & ~15;
+              const uint32_t idq = kv16 == BKV ? id_qk : idesc_f16(128, kv16, false);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 umma_bf16_ss(s_tmem, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2),
-                             id_qk, k > 0);
-              umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), id_qk, 1);
+                             idq, k > 0);
+              umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), idq, 1);
               umma_commit(&s_full[g]);
               umma_commit(&k_empty[kc % KST]);
               if (j == nk - 1) umma_commit(&q_empty[qi]);
@@ -358,8 +361,10 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             tc_fence_after();
             if (elect_one()) {
               const uint32_t va = smem_u32(sm + OFF_V + (vc % VST) * (VA + VB)), vb = va + VA;
+              const int ksteps = (min(BKV, p.Lk - (j - 1) * BKV) + 15) >> 4;  // 16-key steps with keys
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {
+                if (kk >= ksteps) break;
                 const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
                 const uint32_t acc = (j > 1 || kk > 0) ? 1u : 0u;
                 umma_bf16_ss(o_tmem, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
