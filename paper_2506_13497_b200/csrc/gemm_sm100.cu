@@ -422,12 +422,15 @@ DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t*
   const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
   const int row = m0 + rit;
   const int pos = ep.rope ? (row / ep.rope_S) % ep.rope_T : 0;
+  // per-warp staging (32 rows x 144 B, double-buffered) and per-warp TMA stores: the four
+  // epilogue warps never wait for each other
+  const int ew = rit >> 5;
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
-    uint8_t* sb = sE + (cnt & 1) * EpiCfg<144, EPI_QKV>::BUF;
-    const uint32_t sbase = smem_u32(sb) + rit * 144;
-    if (elected) bulk_wait_read<1>();
-    epi_bar();
+    uint8_t* sb = sE + ew * 9216 + (cnt & 1) * 4608;
+    const uint32_t sbase = smem_u32(sb) + lane * 144;
+    if (lane == 0) bulk_wait_read<1>();  // this warp's store of two heads ago has read sb
+    __syncwarp();
     uint32_t r[72];
     tmem_ld_x32(taddr + h * HD, r);
     tmem_ld_x32(taddr + h * HD + 32, r + 32);
@@ -481,9 +484,9 @@ DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t*
                    pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
                    pack_bf16(v[8 * j + 6], v[8 * j + 7]));
     fence_async_smem();
-    epi_bar();
-    if (elected) {
-      tma_store_2d(tmO, sb, c0, m0);
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmO, sb, c0, m0 + ew * 32);
       bulk_commit();
     }
     ++cnt;
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected || (is_resid(EPI) && lane == 0)) bulk_wait<0>();
+    if (elected || ((is_resid(EPI) || EPI == EPI_QKV) && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -863,7 +866,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (elected || (is_resid(EPI) && lane == 0)) bulk_wait<0>();
+    if (elected || ((is_resid(EPI) || EPI == EPI_QKV) && lane == 0)) bulk_wait<0>();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -1018,7 +1021,7 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
         return -3;
       break;
     case EPI_QKV:
-      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, N, ep.ldo, BM, 72, CU_TENSOR_MAP_SWIZZLE_NONE))
+      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, N, ep.ldo, 32, 72, CU_TENSOR_MAP_SWIZZLE_NONE))
         return -3;
       break;
     case EPI_RESID:

@@ -42,3 +42,18 @@ for K, copy in [(1152, True), (1152, False), (4608, False)]:
             tp = t_of(g)
             print(f"K={K} copy={int(copy)} 2cta={two} bn={bn}: resid {t:6.1f} us  plain {tp:6.1f} us", flush=True)
     _lib.lib().ddit_set_gemm_2cta(1)
+
+# QKV epilogue (bias + per-head RMSNorm + RoPE) at the 240p shape, vs the plain bf16 epilogue
+K, N = 1152, 3456
+a = torch.randn(M, K, device=dev).bfloat16()
+w = (torch.randn(N, K, device=dev) / math.sqrt(K)).bfloat16()
+bias = torch.zeros(N, device=dev)
+qw = torch.ones(72, device=dev)
+tab = torch.randn(15, 36, 2, device=dev)
+for two in (1, 0):
+    _lib.lib().ddit_set_gemm_2cta(two)
+    f = lambda: kernels.gemm(a, w, epi=_lib.EPI_QKV, bias=bias, qnorm_w=qw, knorm_w=qw, hidden=1152,
+                             rope_tab=tab, rope_T=15, rope_S=1, bn=144)
+    g = lambda: kernels.gemm(a, w, epi=_lib.EPI_BF16, bias=bias, bn=192)
+    print(f"qkv 2cta={two}: qkv-epilogue {t_of(f):6.1f} us  plain(bn192) {t_of(g):6.1f} us", flush=True)
+_lib.lib().ddit_set_gemm_2cta(1)
