@@ -239,35 +239,57 @@ class B200Executor:
 
     def vae(self, request: RequestState, dit_gpu_ids: tuple[int, ...],
             vae_gpu_ids: tuple[int, ...]) -> float:
-        """DiT -> VAE hand-off: the lowest-id retained GPU gathers the whole latent (K12), then
-        (when a VAE is configured) decodes it to frames on that GPU (K13)."""
+        """DiT -> VAE hand-off and decode on the retained GPUs (K12 + K13). With ``q`` retained
+        GPUs (the policy's vae_dop, reference policies.py:175-190) rank r gathers the latent
+        frames of its block of temporal micro-batches from the DiT T-shards (peer loads) and
+        decodes them (``vae.vae_shard``); the video is the ranks' frames in order. Seconds =
+        max over ranks of gather + decode (device time; ranks of one device are emulated)."""
         live = self.live.pop(request.request_id)
         sh = self._shape(request)
+        q = len(vae_gpu_ids)
+        srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
+        handoffs, decodes, parts, latents = [], [], [], []
+        for rank, gid in enumerate(vae_gpu_ids):
+            dev = self.device_of(gid)
+            if self.vae_cfg is not None:
+                from .vae import vae_shard
+
+                t_lo, t_hi, f_lo, f_hi = vae_shard(self.vae_cfg, sh.T, sh.frames, q, rank)
+            else:  # no decoder: the whole latent goes to the master
+                t_lo, t_hi, f_lo, f_hi = (0, sh.T, 0, sh.frames) if rank == 0 else (0, 0, 0, 0)
+            if t_hi <= t_lo:
+                continue
+            with torch.cuda.device(dev):
+                z = torch.empty((1, self.cfg.in_channels, t_hi - t_lo, *sh.latent[1:]),
+                                device=torch.device("cuda", dev))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                latent_gather(z, t_lo, t_hi, srcs)  # peer loads of the T-shards covering [t_lo, t_hi)
+                b.record()
+                b.synchronize()
+                handoffs.append(a.elapsed_time(b) / 1e3)
+                latents.append(z)
+                if self.vae_cfg is not None:
+                    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s0.record()
+                    video = self._vae(dev).decode(z, f_hi - f_lo, sh.height, sh.width)
+                    s1.record()
+                    s1.synchronize()
+                    decodes.append(s0.elapsed_time(s1) / 1e3)
+                    parts.append(video)
         master = self.device_of(vae_gpu_ids[0])
-        with torch.cuda.device(master):
-            z = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
-            srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            latent_gather(z, 0, sh.T, srcs)  # peer loads of every T-shard into the master
-            b.record()
-            b.synchronize()
-        handoff = a.elapsed_time(b) / 1e3
-        self.final_latents[request.request_id] = z
+        self.final_latents[request.request_id] = (
+            latents[0] if len(latents) == 1
+            else torch.cat([z.to(torch.device("cuda", master)) for z in latents], dim=2))
         self._close(live)
-        decode = 0.0
-        if self.vae_cfg is not None:
-            with torch.cuda.device(master):
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
-                video = self._vae(master).decode(z, sh.frames, sh.height, sh.width)
-                e.record()
-                e.synchronize()
-                decode = s.elapsed_time(e) / 1e3
-            if self.keep_videos:
-                self.videos[request.request_id] = video
-        self.vae_seconds.append((request.request_id, handoff, decode))
-        return handoff + decode
+        if self.keep_videos and parts:
+            self.videos[request.request_id] = (
+                parts[0] if len(parts) == 1
+                else torch.cat([v.to(torch.device("cuda", master)) for v in parts], dim=2))
+        decodes += [0.0] * (len(handoffs) - len(decodes))
+        slowest = max(range(len(handoffs)), key=lambda i: handoffs[i] + decodes[i])
+        self.vae_seconds.append((request.request_id, handoffs[slowest], decodes[slowest]))
+        return handoffs[slowest] + decodes[slowest]
 
     # ---------------------------------------------------------------- internals
     def _run_step(self, live: _Live, step: int) -> float:

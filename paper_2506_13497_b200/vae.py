@@ -242,6 +242,19 @@ class VAEDecoder:
         return self.spatial_decode(x4, height, width)
 
 
+def vae_shard(cfg: VAEConfig, t_latent: int, frames: int, dop: int, rank: int) -> tuple[int, int, int, int]:
+    """VAE DoP: rank ``rank`` of ``dop`` decodes a contiguous block of the temporal VAE's
+    micro-batches (``micro_z`` latent frames -> ``micro_frame_size`` video frames each). The
+    micro-batches are decoded independently (VideoAutoencoderPipeline.decode) and the spatial
+    decoder is per frame, so the ranks need no halo and their frames concatenate to the DoP-1
+    video exactly. Returns (latent t_lo, t_hi, frame f_lo, f_hi); empty ranges have lo == hi."""
+    chunks = -(-t_latent // cfg.micro_z)
+    per = -(-chunks // dop)
+    c_lo, c_hi = min(rank * per, chunks), min((rank + 1) * per, chunks)
+    return (min(c_lo * cfg.micro_z, t_latent), min(c_hi * cfg.micro_z, t_latent),
+            min(c_lo * cfg.micro_frame_size, frames), min(c_hi * cfg.micro_frame_size, frames))
+
+
 def vae_flops(cfg: VAEConfig, frames: int, t_latent: int, h: int, w: int) -> float:
     """Algorithmic FLOPs of one decode (tensor-core convs + attention), for the roofline."""
     fl = 0.0

@@ -110,3 +110,47 @@ def test_engine_with_vae_decode(cuda):
     torch.cuda.synchronize()
     assert torch.equal(video, ref)
     assert ex.vae_seconds[0][2] > 0
+
+
+@pytest.mark.parametrize("vae_dop", [2, 4])
+def test_vae_dop_splits_micro_batches(cuda, vae_dop):
+    """VAE DoP q: the ranks' blocks of temporal micro-batches decode to the DoP-1 video exactly."""
+    from paper_2506_13497_b200 import vae_weights as vw
+    from paper_2506_13497_b200.vae import VAEDecoder, vae_shard
+
+    cfg = vw.TINY_VAE
+    W = vw.init_vae_weights(cfg)
+    T, frames, h, w = 15, 51, 4, 6
+    z = torch.randn(1, 4, T, h, w, generator=torch.Generator().manual_seed(3)).to(cuda)
+    dec = VAEDecoder(cfg, W, cuda)
+    full = dec.decode(z, frames, 8 * h, 8 * w)
+    parts = []
+    for r in range(vae_dop):
+        t_lo, t_hi, f_lo, f_hi = vae_shard(cfg, T, frames, vae_dop, r)
+        if t_hi > t_lo:
+            parts.append(dec.decode(z[:, :, t_lo:t_hi].contiguous(), f_hi - f_lo, 8 * h, 8 * w))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, dim=2), full)
+
+
+def test_engine_with_vae_dop2(cuda):
+    """Decoupled DiT(DoP 4) -> VAE(DoP 2) (BASELINE config 4): the policy keeps the two lowest
+    GPUs, each decodes its micro-batches; the video equals decoding the DoP-1 latent."""
+    from paper_2506_13497_b200 import sched, shapes, weights, vae_weights as vw
+    from paper_2506_13497_b200.executor import B200Executor
+    from paper_2506_13497_b200.vae import VAEDecoder
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W = weights.init_weights(cfg, seed=3)
+    VW = vw.init_vae_weights(vw.TINY_VAE)
+    ex = B200Executor(cfg, W, num_steps=2, vae_cfg=vw.TINY_VAE, vae_weights=VW, keep_videos=True)
+    t = sched.load_profiles(_profile_doc())
+    dt = sched.derive_dop_table(t, vae_dop=2)
+    wl = [sched.ArrivalRecord(0, 0.0, "144p", 2)]  # 144p x 51 frames: 3 micro-batches
+    res = sched.Simulation(sched.ClusterTopology(1, 4), t, dt, wl, sched.GreedyPolicy(dt), executor=ex).run()
+    dc = [r for r in res.trace if r.kind == "dit_complete"][0]
+    assert dc.gpu_ids == (0, 1)  # retained: the two lowest of the DiT group (0..3)
+    sh = shapes.shape_of("144p")
+    ref = VAEDecoder(vw.TINY_VAE, VW, cuda).decode(ex.final_latents[0], sh.frames, sh.height, sh.width)
+    torch.cuda.synchronize()
+    assert torch.equal(ex.videos[0], ref)

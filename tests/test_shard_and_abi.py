@@ -94,3 +94,21 @@ def test_c_abi_rejects_bad_dop():
     out = [ctypes.c_int() for _ in range(4)]
     rc = L.lib().ddit_request_shard(None, ctypes.byref(d), *[ctypes.byref(o) for o in out])
     assert rc == L.DDIT_E_LOOKUP
+
+
+@pytest.mark.parametrize("T,frames", [(15, 51), (30, 102), (4, 16), (5, 17), (2, 5)])
+@pytest.mark.parametrize("dop", [1, 2, 4])
+def test_vae_shard_partitions_micro_batches(T, frames, dop):
+    """VAE DoP split (vae.vae_shard): contiguous blocks of whole temporal micro-batches whose latent
+    and frame ranges tile [0, T) and [0, frames) in rank order."""
+    from paper_2506_13497_b200.vae import vae_shard
+    from paper_2506_13497_b200.vae_weights import OPENSORA_VAE as cfg
+
+    t_next = f_next = 0
+    for r in range(dop):
+        t_lo, t_hi, f_lo, f_hi = vae_shard(cfg, T, frames, dop, r)
+        assert (t_lo, f_lo) == (t_next, f_next)
+        assert (t_lo == T or t_lo % cfg.micro_z == 0) and (t_hi == T or t_hi % cfg.micro_z == 0)
+        assert (t_hi > t_lo) == (f_hi > f_lo)
+        t_next, f_next = t_hi, f_hi
+    assert (t_next, f_next) == (T, frames)
