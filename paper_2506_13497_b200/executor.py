@@ -255,6 +255,9 @@ class B200Executor:
                 from .vae import vae_shard
 
                 t_lo, t_hi, f_lo, f_hi = vae_shard(self.vae_cfg, sh.T, sh.frames, q, rank)
+                mf = self.vae_cfg.micro_frame_size
+                f0 = t_lo // self.vae_cfg.micro_z * mf  # first frame of the rank's micro-batches
+                part_frames = min(-(-(t_hi - t_lo) // self.vae_cfg.micro_z) * mf, sh.frames - f0)
             else:  # no decoder: the whole latent goes to the master
                 t_lo, t_hi, f_lo, f_hi = (0, sh.T, 0, sh.frames) if rank == 0 else (0, 0, 0, 0)
             if t_hi <= t_lo:
@@ -272,15 +275,19 @@ class B200Executor:
                 if self.vae_cfg is not None:
                     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     s0.record()
-                    video = self._vae(dev).decode(z, f_hi - f_lo, sh.height, sh.width)
+                    video = self._vae(dev).decode(z, part_frames, sh.height, sh.width,
+                                                  frames=(f_lo - f0, f_hi - f0))
                     s1.record()
                     s1.synchronize()
                     decodes.append(s0.elapsed_time(s1) / 1e3)
                     parts.append(video)
         master = self.device_of(vae_gpu_ids[0])
-        self.final_latents[request.request_id] = (
-            latents[0] if len(latents) == 1
-            else torch.cat([z.to(torch.device("cuda", master)) for z in latents], dim=2))
+        if q == 1 or self.vae_cfg is None:
+            self.final_latents[request.request_id] = latents[0]
+        else:  # the ranks' latent ranges overlap at micro-batch boundaries
+            zf = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
+            latent_gather(zf, 0, sh.T, srcs)
+            self.final_latents[request.request_id] = zf
         self._close(live)
         if self.keep_videos and parts:
             self.videos[request.request_id] = (

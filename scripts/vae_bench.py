@@ -28,3 +28,24 @@ ms = s.elapsed_time(e)
 fl = vae_flops(cfg, sh.frames, sh.T, *sh.latent[1:])
 print(f"VAE decode {label}x{sh.frames}: {ms:.1f} ms, {fl / 1e12:.1f} TFLOP -> {fl / ms / 1e9:.0f} TFLOP/s, "
       f"launches {dec.launches - n0}, out {tuple(out.shape)} finite={torch.isfinite(out).all().item()}")
+# VAE DoP q: each rank decodes its block of frames (vae.vae_shard); the DoP-q
+# decode latency is the slowest rank's (ranks run one after another on this GPU)
+from paper_2506_13497_b200.vae import vae_shard  # noqa: E402
+
+for q in (2, 4):
+    per = []
+    for r in range(q):
+        t_lo, t_hi, f_lo, f_hi = vae_shard(cfg, sh.T, sh.frames, q, r)
+        if f_hi <= f_lo:
+            continue
+        zp = z[:, :, t_lo:t_hi].contiguous()
+        f0 = t_lo // cfg.micro_z * cfg.micro_frame_size
+        nf = min(-(-(t_hi - t_lo) // cfg.micro_z) * cfg.micro_frame_size, sh.frames - f0)
+        dec.decode(zp, nf, sh.height, sh.width, frames=(f_lo - f0, f_hi - f0))
+        s.record()
+        dec.decode(zp, nf, sh.height, sh.width, frames=(f_lo - f0, f_hi - f0))
+        e.record()
+        torch.cuda.synchronize()
+        per.append(s.elapsed_time(e))
+    print(f"VAE decode {label}x{sh.frames} at VAE DoP {q}: per-rank ms {[round(x, 1) for x in per]} "
+          f"-> {max(per):.1f} ms")

@@ -114,7 +114,8 @@ def test_engine_with_vae_decode(cuda):
 
 @pytest.mark.parametrize("vae_dop", [2, 4])
 def test_vae_dop_splits_micro_batches(cuda, vae_dop):
-    """VAE DoP q: the ranks' blocks of temporal micro-batches decode to the DoP-1 video exactly."""
+    """VAE DoP q: each rank's frame block (temporal micro-batches it overlaps, spatial decode of
+    its own frames) concatenates to the DoP-1 video exactly."""
     from paper_2506_13497_b200 import vae_weights as vw
     from paper_2506_13497_b200.vae import VAEDecoder, vae_shard
 
@@ -127,8 +128,11 @@ def test_vae_dop_splits_micro_batches(cuda, vae_dop):
     parts = []
     for r in range(vae_dop):
         t_lo, t_hi, f_lo, f_hi = vae_shard(cfg, T, frames, vae_dop, r)
-        if t_hi > t_lo:
-            parts.append(dec.decode(z[:, :, t_lo:t_hi].contiguous(), f_hi - f_lo, 8 * h, 8 * w))
+        if f_hi > f_lo:
+            f0 = t_lo // cfg.micro_z * cfg.micro_frame_size
+            nf = min(-(-(t_hi - t_lo) // cfg.micro_z) * cfg.micro_frame_size, frames - f0)
+            parts.append(dec.decode(z[:, :, t_lo:t_hi].contiguous(), nf, 8 * h, 8 * w,
+                                    frames=(f_lo - f0, f_hi - f0)))
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, dim=2), full)
 

@@ -99,16 +99,17 @@ def test_c_abi_rejects_bad_dop():
 @pytest.mark.parametrize("T,frames", [(15, 51), (30, 102), (4, 16), (5, 17), (2, 5)])
 @pytest.mark.parametrize("dop", [1, 2, 4])
 def test_vae_shard_partitions_micro_batches(T, frames, dop):
-    """VAE DoP split (vae.vae_shard): contiguous blocks of whole temporal micro-batches whose latent
-    and frame ranges tile [0, T) and [0, frames) in rank order."""
+    """VAE DoP split (vae.vae_shard): frame blocks tile [0, frames) in rank order; each rank's
+    latent range is whole micro-batches covering exactly the micro-batches its frames fall in."""
     from paper_2506_13497_b200.vae import vae_shard
     from paper_2506_13497_b200.vae_weights import OPENSORA_VAE as cfg
 
-    t_next = f_next = 0
+    mz, mf = cfg.micro_z, cfg.micro_frame_size
+    f_next = 0
     for r in range(dop):
         t_lo, t_hi, f_lo, f_hi = vae_shard(cfg, T, frames, dop, r)
-        assert (t_lo, f_lo) == (t_next, f_next)
-        assert (t_lo == T or t_lo % cfg.micro_z == 0) and (t_hi == T or t_hi % cfg.micro_z == 0)
-        assert (t_hi > t_lo) == (f_hi > f_lo)
-        t_next, f_next = t_hi, f_hi
-    assert (t_next, f_next) == (T, frames)
+        assert f_lo == f_next
+        if f_hi > f_lo:
+            assert t_lo == f_lo // mf * mz and t_hi == min(-(-f_hi // mf) * mz, T)
+        f_next = f_hi
+    assert f_next == frames
