@@ -23,3 +23,17 @@ def test_multiprocess_group_matches_dop1(cuda, dop, fused):
     print(res.stdout[-3000:], res.stderr[-3000:])
     assert res.returncode == 0
     assert "PASS" in res.stdout
+
+
+def test_multiprocess_group_ranks_without_frames(cuda):
+    """DoP 8 over T = 4 latent frames (144p-16f): ranks 4..7 own no frames in the spatial phase,
+    run no fc2 GEMM there and must still publish their exchange flags (stand-alone kernel) while
+    the other ranks' fused GEMM epilogues signal -- real processes, flag barrier, CUDA graphs."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29650", str(ROOT / "scripts" / "group_check.py"),
+           "144p-16f"]
+    env = dict(os.environ, OMP_NUM_THREADS="1", DDIT_FUSED_XCH="1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    print(res.stdout[-3000:], res.stderr[-3000:])
+    assert res.returncode == 0
+    assert "PASS" in res.stdout

@@ -71,12 +71,14 @@ def test_xl2_width_step_matches_oracle(cuda, label):
 
 
 @pytest.mark.parametrize("fused", [1, 0], ids=["fused-xch", "xch-kernel"])
-@pytest.mark.parametrize("label", ["144p", "240p"])
+@pytest.mark.parametrize("label", ["144p", "240p", "144p-16f"])
 @pytest.mark.parametrize("dop", [2, 4, 8])
 def test_virtual_dop_matches_dop1(cuda, dop, label, fused):
     """DoP-P shards + exchange (virtual ranks on one device) reproduce the DoP-1 step, with the
     exchange fused into the fc2 GEMM epilogue (peer stores) or as the separate kernel.
-    144p: T=15 (ragged T shards), S=144; 240p: S=405 (ragged S shards at every P)."""
+    144p: T=15 (ragged T shards), S=144; 240p: S=405 (ragged S shards at every P);
+    144p-16f: T=4, so at P=8 ranks 4..7 own no frames (no spatial-phase GEMM: they signal through
+    the stand-alone exchange kernel)."""
     from paper_2506_13497_b200 import _lib, weights
     from paper_2506_13497_b200.stdit import STDiTModel, StepRequest, VirtualGroup
 
