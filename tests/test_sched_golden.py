@@ -116,3 +116,30 @@ def test_simulation_replay(idx):
     got = [[r.request_id, r.resolution, h(r.arrival), h(r.start), h(r.finish), h(r.gpu_seconds),
             [[h(a), w] for a, w in r.dop_history]] for r in res.requests]
     assert got == case["requests"]
+
+
+def test_reference_crosscheck_of_b200_profile():
+    """The dit-profile/1 document measured on a B200 (profiles/r01_trace_replay_c5.json), fed to
+    the unmodified reference simulator (scripts/reference_crosscheck.py, run where
+    /root/reference exists), and to this repo's scheduler give the same config-5 predictions."""
+    import json
+    from pathlib import Path
+
+    from paper_2506_13497_b200 import sched
+
+    root = Path(__file__).resolve().parents[1]
+    run = json.loads((root / "profiles" / "r01_trace_replay_c5.json").read_text())
+    ref = json.loads((root / "profiles" / "r01_reference_crosscheck.json").read_text())
+    table = sched.load_profiles(run["profile"])
+    dt = sched.derive_dop_table(table)
+    assert dict(dt.by_resolution) == ref["b_values"]
+    mix = {k: 1 / 3 for k in ("144p", "240p", "360p")}
+    for rate, rec in ref["rates"].items():
+        spec = sched.WorkloadSpec(proportions=mix, total_requests=run["requests"],
+                                  arrival_rate=float(rate), seed=0, denoise_steps=run["denoise_steps"])
+        res = sched.Simulation(sched.ClusterTopology(1, 8), table, dt, sched.generate(spec),
+                               sched.GreedyPolicy(dt)).run()
+        m = sched.compute_metrics(res)
+        assert round(m.avg_latency, 4) == rec["reference"]["avg_latency_s"]
+        assert round(m.p99_latency, 4) == rec["reference"]["p99_latency_s"]
+        assert round(m.cumulative_occupancy, 3) == rec["reference"]["gpu_seconds"]
