@@ -47,7 +47,7 @@ constexpr int OFF_K = OFF_Q + 4 * QT;              // KST K stages
 constexpr int OFF_V = OFF_K + KST * (KA + KB);     // VST V stages
 constexpr int OFF_P = OFF_V + VST * (VA + VB);     // P per group (also its O store staging)
 constexpr int OFF_BAR = OFF_P + 2 * PBUF;
-constexpr int NBAR = 28;
+constexpr int NBAR = 30;
 constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
 constexpr uint32_t TM_S0 = 0, TM_O0 = 256;  // group g: S at TM_S0 + 128 g, O at TM_O0 + 128 g
 constexpr float RESCALE_LOG2 = 8.0f;
@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   uint64_t* p_full = bars + 20;   // [group]
   uint64_t* pv_done = bars + 22;  // [group]
   uint64_t* o_free = bars + 24;   // [group]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* exp_tok = bars + 26;  // [group]: the group may run its exps phase (MUFU turn)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
 
   const int warp = warp_id(), lane = lane_id();
   const int nk = (p.Lk + BKV - 1) / BKV;
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_free[i], 4);
+      mbar_init(&exp_tok[i], 4);
     }
     fence_barrier_init();
   }
@@ -392,7 +394,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
     const int bar_id = 1 + g;
     const bool elected = quarter == 0 && lane == 0;
     uint8_t* pbuf = sm + OFF_P + g * PBUF;
-    int n = 0;  // tiles processed by this group
+    int n = 0;   // tiles processed by this group
+    int tk = 0;  // exps phases run under the MUFU token (tiles of units with both groups)
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       int pr, head, seq;
       bool has1;
@@ -440,6 +443,10 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           m = m_new;
           l *= alpha;
         }
+        // MUFU turn: the two groups' exps phases alternate (g0 tile j, g1 tile j, g0 tile j+1, ...)
+        // so each runs at the full SFU rate while the other does its max / P stores / waits,
+        // instead of both contending in phase
+        if (has1) mbar_wait(&exp_tok[g], (tk & 1) ^ (g == 0 ? 1 : 0));
         // exps first (packed bf16 P kept in the consumed s[] registers: chunk c -> s[4c..4c+3]),
         // so the MUFU work overlaps the tensor core finishing PV_{j-1}
         const float neg_m = -m;
@@ -486,6 +493,11 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
               for (int e = 0; e < 4; ++e) s[4 * c + e] = 0u;
             }
           }
+        }
+        if (has1) {  // hand the MUFU turn to the other group
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&exp_tok[g ^ 1]);
+          ++tk;
         }
         if (j > 0) {
           // PV of the previous tile done: P buffer free, O complete through tile j-1
