@@ -238,28 +238,45 @@ int build_tables(float* pos, int h, int w, int C, float scale, float base_size, 
 // ------------------------------------------------------------------ step entry (K9)
 // x[b][t][s][c] = bias[c] + sum_{ci,dh,dw} Wp[c][ci][dh][dw] z[ci][t][2i+dh][2j+dw] + pos[s][c]
 // z: the local T-shard [Cin][Tl][Hl][Wl] fp32 (zero outside Hl x Wl); same x for all nb copies.
-__global__ void __launch_bounds__(256)
+// One thread per output channel c (its K <= 16 weights in registers), a block per 128 channels x
+// 32 tokens: the token patches are staged in smem once per block, the pos-embed row and the
+// output row are coalesced over c. (One block per token re-read all C x K weights per token.)
+namespace pe {
+constexpr int CPB = 128, TPB = 32;
+}
+
+__global__ void __launch_bounds__(pe::CPB)
     patch_embed_kernel(const float* __restrict__ z, const float* __restrict__ Wp,
                        const float* __restrict__ bp, const float* __restrict__ pos,
                        float* __restrict__ x, int Tl, int Hl, int Wl, int h, int w, int C,
                        int Cin, int nb) {
-  const int tok = blockIdx.x;  // t * S + s
-  const int S = h * w;
-  const int t = tok / S, s = tok % S;
-  const int i = s / w, j = s % w;
-  __shared__ float patch[64];
-  if (threadIdx.x < Cin * 4) {
-    const int ci = threadIdx.x / 4, dh = (threadIdx.x / 2) % 2, dw = threadIdx.x % 2;
-    const int y = 2 * i + dh, xx = 2 * j + dw;
-    patch[threadIdx.x] =
-        (y < Hl && xx < Wl) ? z[(((size_t)ci * Tl + t) * Hl + y) * Wl + xx] : 0.f;
+  const int S = h * w, ntok = Tl * S, K = Cin * 4;
+  const int c = blockIdx.x * pe::CPB + threadIdx.x;
+  const int tok0 = blockIdx.y * pe::TPB;
+  __shared__ float patch[pe::TPB][16];
+  for (int e = threadIdx.x; e < pe::TPB * K; e += pe::CPB) {
+    const int tt = e / K, k = e % K, tok = tok0 + tt;
+    float v = 0.f;
+    if (tok < ntok) {
+      const int t = tok / S, sidx = tok % S, i = sidx / w, j = sidx % w;
+      const int ci = k / 4, y = 2 * i + (k / 2) % 2, xx = 2 * j + k % 2;
+      if (y < Hl && xx < Wl) v = z[(((size_t)ci * Tl + t) * Hl + y) * Wl + xx];
+    }
+    patch[tt][k] = v;
   }
   __syncthreads();
-  const int K = Cin * 4;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float acc = bp[c] + pos[(size_t)s * C + c];
-    const float* wr = Wp + (size_t)c * K;
-    for (int k = 0; k < K; ++k) acc += wr[k] * patch[k];
+  if (c >= C) return;
+  float wv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) wv[k] = k < K ? Wp[(size_t)c * K + k] : 0.f;
+  const float bias = bp[c];
+  for (int tt = 0; tt < pe::TPB; ++tt) {
+    const int tok = tok0 + tt;
+    if (tok >= ntok) break;
+    float acc = bias + pos[(size_t)(tok % S) * C + c];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < K) acc += wv[k] * patch[tt][k];
     for (int b = 0; b < nb; ++b) x[((size_t)b * Tl * S + tok) * C + c] = acc;
   }
 }
@@ -267,7 +284,9 @@ __global__ void __launch_bounds__(256)
 int patch_embed(const float* z, const float* Wp, const float* bp, const float* pos, float* x, int Tl,
                 int Hl, int Wl, int h, int w, int C, int Cin, int nb, cudaStream_t s) {
   if (Tl <= 0) return 0;
-  patch_embed_kernel<<<Tl * h * w, 256, 0, s>>>(z, Wp, bp, pos, x, Tl, Hl, Wl, h, w, C, Cin, nb);
+  if (Cin * 4 > 16) return -2;
+  const dim3 grid((C + pe::CPB - 1) / pe::CPB, (Tl * h * w + pe::TPB - 1) / pe::TPB);
+  patch_embed_kernel<<<grid, pe::CPB, 0, s>>>(z, Wp, bp, pos, x, Tl, Hl, Wl, h, w, C, Cin, nb);
   return 0;
 }
 
@@ -276,78 +295,105 @@ int patch_embed(const float* z, const float* Wp, const float* bp, const float* p
 //   y_b = LN(x_b) * (1 + scale_b) + shift_b ;  o_b[f] = Wf[f] . y_b + bf[f]
 // for the 16 features f = (hp*2 + wp)*out_ch + c with c < Cin (the sigma half is unused);
 //   v = o_uncond + g (o_cond - o_uncond);  z[c][t][2i+hp][2j+wp] += v * dt.
-__global__ void __launch_bounds__(128)
+// Persistent CTAs keep the 16 used rows of Wf and both rows of the final modulation in smem;
+// one warp per token (its two rows in registers, float4 loads). (A CTA per token re-read the
+// 74 KB of Wf rows from L2 for every token.)
+namespace fl {
+constexpr int WARPS = 8, MAXV = 12;  // C <= 32 * 4 * MAXV
+}
+
+__global__ void __launch_bounds__(fl::WARPS * 32)
     final_layer_kernel(const float* __restrict__ x, const float* __restrict__ fin,
                        const float* __restrict__ Wf, const float* __restrict__ bf,
                        float* __restrict__ z, int Tl, int Hl, int Wl, int h, int w, int C,
                        int Cin, int out_ch, float guidance, float dt, float eps) {
-  const int tok = blockIdx.x;
-  const int S = h * w;
-  const int t = tok / S, s = tok % S;
-  const int i = s / w, j = s % w;
+  extern __shared__ __align__(16) float fl_smem[];
+  const int nf = 4 * Cin;                   // used features (<= 16)
+  float* wsm = fl_smem;                     // [nf][C]
+  float* msm = fl_smem + (size_t)nf * C;    // [2 b][shift C, scale C]
+  for (int e = threadIdx.x; e < nf * C; e += blockDim.x) {
+    const int f16 = e / C, cc = e % C;
+    wsm[e] = Wf[(size_t)((f16 / Cin) * out_ch + f16 % Cin) * C + cc];
+  }
+  for (int e = threadIdx.x; e < 4 * C; e += blockDim.x) msm[e] = fin[e];
+  __syncthreads();
+  const int S = h * w, ntok = Tl * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ float red[2][4][2];
-  __shared__ float stats[2][2];
-  __shared__ float outv[2][16];
-  // LayerNorm stats for the two CFG rows
-  for (int b = 0; b < 2; ++b) {
-    const float* xr = x + ((size_t)b * Tl * S + tok) * C;
-    float sm = 0.f, sq = 0.f;
-    for (int c = threadIdx.x; c < C; c += 128) {
-      const float v = xr[c];
-      sm += v;
-      sq += v * v;
-    }
-    sm = warp_sum(sm);
-    sq = warp_sum(sq);
-    if (lane == 0) {
-      red[b][warp][0] = sm;
-      red[b][warp][1] = sq;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 2) {
-    const int b = threadIdx.x;
-    float sm = 0.f, sq = 0.f;
-    for (int k = 0; k < 4; ++k) {
-      sm += red[b][k][0];
-      sq += red[b][k][1];
-    }
-    const float mean = sm / C;
-    const float var = fmaxf(sq / C - mean * mean, 0.f);
-    stats[b][0] = mean;
-    stats[b][1] = rsqrtf(var + eps);
-  }
-  __syncthreads();
-  // 32 dot products (16 features x 2 rows); warp w takes features 4w..4w+3
-  for (int fi = 0; fi < 4; ++fi) {
-    const int f16 = warp * 4 + fi;           // (hp*2+wp)*Cin + c
-    const int pidx = f16 / Cin, c = f16 % Cin;
-    const int feat = pidx * out_ch + c;
-    const float* wr = Wf + (size_t)feat * C;
+  const int nv = C >> 2;
+  for (int tok = blockIdx.x * fl::WARPS + warp; tok < ntok; tok += gridDim.x * fl::WARPS) {
+    float o[2];  // this lane's feature ((lane >> 1) & 15) for the two CFG rows
+#pragma unroll
     for (int b = 0; b < 2; ++b) {
-      const float* xr = x + ((size_t)b * Tl * S + tok) * C;
-      const float* sh = fin + (size_t)b * 2 * C;
-      const float* sc = sh + C;
-      float acc = 0.f;
-      for (int cc = lane; cc < C; cc += 32) {
-        const float yv = (xr[cc] - stats[b][0]) * stats[b][1] * (1.f + sc[cc]) + sh[cc];
-        acc += wr[cc] * yv;
+      const float4* xr = reinterpret_cast<const float4*>(x + ((size_t)b * Tl * S + tok) * C);
+      float4 v[fl::MAXV];
+      float sm = 0.f, sq = 0.f;
+#pragma unroll
+      for (int k = 0; k < fl::MAXV; ++k) {
+        const int q = lane + 32 * k;
+        if (q < nv) {
+          v[k] = __ldcs(xr + q);
+          sm += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+          sq += (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w);
+        }
       }
-      acc = warp_sum(acc);
-      if (lane == 0) outv[b][f16] = acc + bf[feat];
+      sm = warp_sum(sm);
+      sq = warp_sum(sq);
+      const float mean = sm / C;
+      const float rstd = rsqrtf(fmaxf(sq / C - mean * mean, 0.f) + eps);
+      const float4* sh = reinterpret_cast<const float4*>(msm + (size_t)b * 2 * C);
+      const float4* sc = reinterpret_cast<const float4*>(msm + (size_t)b * 2 * C + C);
+#pragma unroll
+      for (int k = 0; k < fl::MAXV; ++k) {
+        const int q = lane + 32 * k;
+        if (q < nv) {
+          const float4 a = sh[q], g = sc[q];
+          v[k].x = (v[k].x - mean) * rstd * (1.f + g.x) + a.x;
+          v[k].y = (v[k].y - mean) * rstd * (1.f + g.y) + a.y;
+          v[k].z = (v[k].z - mean) * rstd * (1.f + g.z) + a.z;
+          v[k].w = (v[k].w - mean) * rstd * (1.f + g.w) + a.w;
+        }
+      }
+      float part[16];
+#pragma unroll
+      for (int f = 0; f < 16; ++f) {
+        part[f] = 0.f;
+        if (f >= nf) continue;
+        const float4* wr = reinterpret_cast<const float4*>(wsm + (size_t)f * C);
+#pragma unroll
+        for (int k = 0; k < fl::MAXV; ++k) {
+          const int q = lane + 32 * k;
+          if (q < nv) {
+            const float4 ww = wr[q];
+            part[f] += (v[k].x * ww.x + v[k].y * ww.y) + (v[k].z * ww.z + v[k].w * ww.w);
+          }
+        }
+      }
+      // reduce-scatter of the 16 partial sums over the warp: 8 + 4 + 2 + 1 shuffles leave lane l
+      // with feature f(l) = bits 4..1 of l summed over 16 lanes, one more shuffle completes it
+#pragma unroll
+      for (int hbit = 8; hbit >= 1; hbit >>= 1) {
+        const bool up = lane & (2 * hbit);
+#pragma unroll
+        for (int i = 0; i < hbit; ++i) {
+          const float send = up ? part[i] : part[i + hbit];
+          const float keep = up ? part[i + hbit] : part[i];
+          part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * hbit);
+        }
+      }
+      o[b] = part[0] + __shfl_xor_sync(0xffffffffu, part[0], 1);
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < 4 * Cin) {
-    const int f16 = threadIdx.x;
-    const int pidx = f16 / Cin, c = f16 % Cin;
-    const int hp = pidx / 2, wp = pidx % 2;
-    const int yy = 2 * i + hp, xx = 2 * j + wp;
-    if (yy < Hl && xx < Wl) {
-      const float v = outv[1][f16] + guidance * (outv[0][f16] - outv[1][f16]);
-      float* zp = z + (((size_t)c * Tl + t) * Hl + yy) * Wl + xx;
-      *zp = *zp + v * dt;
+    const int t = tok / S, sidx = tok % S, i = sidx / w, j = sidx % w;
+    const int f = (lane >> 1) & 15;
+    if ((lane & 1) == 0 && f < nf) {
+      const int pidx = f / Cin, c = f % Cin;
+      const int feat = pidx * out_ch + c;
+      const int yy = 2 * i + pidx / 2, xx = 2 * j + pidx % 2;
+      if (yy < Hl && xx < Wl) {
+        const float oc = o[0] + bf[feat], ou = o[1] + bf[feat];
+        const float vv = ou + guidance * (oc - ou);
+        float* zp = z + (((size_t)c * Tl + t) * Hl + yy) * Wl + xx;
+        *zp = *zp + vv * dt;
+      }
     }
   }
 }
@@ -356,9 +402,20 @@ int final_layer(const float* x, const float* fin, const float* Wf, const float* 
                 int Hl, int Wl, int h, int w, int C, int Cin, int out_ch, float guidance, float dt,
                 float eps, cudaStream_t s) {
   if (Tl <= 0) return 0;
-  if (4 * Cin > 16) return -2;
-  final_layer_kernel<<<Tl * h * w, 128, 0, s>>>(x, fin, Wf, bf, z, Tl, Hl, Wl, h, w, C, Cin, out_ch,
-                                                 guidance, dt, eps);
+  if (4 * Cin > 16 || C % 4 || C > 32 * 4 * fl::MAXV) return -2;
+  const size_t smem = ((size_t)4 * Cin * C + 4 * C) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(final_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ntok = Tl * h * w;
+  const int blocks = (ntok + fl::WARPS - 1) / fl::WARPS;
+  final_layer_kernel<<<blocks < 2 * sms ? blocks : 2 * sms, fl::WARPS * 32, smem, s>>>(
+      x, fin, Wf, bf, z, Tl, Hl, Wl, h, w, C, Cin, out_ch, guidance, dt, eps);
   return 0;
 }
 
