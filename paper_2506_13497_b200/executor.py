@@ -240,10 +240,11 @@ class B200Executor:
     def vae(self, request: RequestState, dit_gpu_ids: tuple[int, ...],
             vae_gpu_ids: tuple[int, ...]) -> float:
         """DiT -> VAE hand-off and decode on the retained GPUs (K12 + K13). With ``q`` retained
-        GPUs (the policy's vae_dop, reference policies.py:175-190) rank r gathers the latent
-        frames of its block of temporal micro-batches from the DiT T-shards (peer loads) and
-        decodes them (``vae.vae_shard``); the video is the ranks' frames in order. Seconds =
-        max over ranks of gather + decode (device time; ranks of one device are emulated)."""
+        GPUs (the policy's vae_dop, reference policies.py:175-190) rank r owns an even block of
+        video frames: it gathers the latent frames of the temporal micro-batches those frames
+        fall in from the DiT T-shards (peer loads) and decodes only its frames
+        (``vae.vae_shard``); the video is the ranks' frames in order. Seconds = max over ranks of
+        gather + decode (device time; ranks of one device are emulated)."""
         live = self.live.pop(request.request_id)
         sh = self._shape(request)
         q = len(vae_gpu_ids)
