@@ -173,10 +173,17 @@ def run_ours(args) -> dict | None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (use torchrun for N>1)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank; on a box with fewer GPUs than ranks (a 1-GPU test box) the ranks share
+    # devices round-robin and the plumbing falls back to gloo (NCCL needs a GPU per rank)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
+    shared_gpus = world > ndev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpus:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = weights.XL2
     sh = shapes.shape_of(args.label)
     # random-init XL/2 weights on the device (same seed on every rank)
@@ -257,10 +264,11 @@ def run_ours(args) -> dict | None:
     e2e_ms = e0.elapsed_time(e1) / args.steps
     zbytes = z.numel() * 4
 
-    t_step = torch.tensor([ms_step, e2e_ms], device=dev)
+    cdev = torch.device("cpu") if shared_gpus else dev
+    t_step = torch.tensor([ms_step, e2e_ms], device=cdev)
     if world > 1:
         dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
-        zb = torch.tensor([zbytes], device=dev, dtype=torch.float64)
+        zb = torch.tensor([zbytes], device=cdev, dtype=torch.float64)
         dist.all_reduce(zb)
         zbytes = int(zb.item())
     ms_step, e2e_ms = t_step.tolist()
@@ -302,7 +310,9 @@ def run_ours(args) -> dict | None:
                         f"(latent {sh.T}x{sh.latent[1]}x{sh.latent[2]}, {sh.N} tokens/sample), "
                         "CFG batch 2, RFLOW Euler update",
             "dop": world,
-            "parallelism": f"sp{world} (DSP T-shard/S-shard all-to-all)" if world > 1 else "none",
+            "parallelism": (f"sp{world} (DSP T-shard/S-shard all-to-all, fused into the fc2 GEMM)"
+                            + (f"; {world} ranks sharing {ndev} GPU(s): not a scaling number"
+                               if shared_gpus else "")) if world > 1 else "none",
             "step_tflop": round(fl["total"] / 1e12, 3),
             "l2": "inputs larger than L2 (2.2 GB of bf16 weights + >1 GB activations per step)",
             "launch": "CUDA graph per step index (captured before the timed region)" if use_graph
