@@ -47,7 +47,7 @@ constexpr int OFF_K = OFF_Q + 4 * QT;              // KST K stages
 constexpr int OFF_V = OFF_K + KST * (KA + KB);     // VST V stages
 constexpr int OFF_P = OFF_V + VST * (VA + VB);     // P per group (also its O store staging)
 constexpr int OFF_BAR = OFF_P + 2 * PBUF;
-constexpr int NBAR = 30;
+constexpr int NBAR = 32;
 constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
 constexpr uint32_t TM_S0 = 0, TM_O0 = 256;  // group g: S at TM_S0 + 128 g, O at TM_O0 + 128 g
 constexpr float RESCALE_LOG2 = 8.0f;
@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   uint64_t* pv_done = bars + 22;  // [group]
   uint64_t* o_free = bars + 24;   // [group]
   uint64_t* exp_tok = bars + 26;  // [group]: the group may run its exps phase (MUFU turn)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+  uint64_t* v_ready = bars + 28;  // [VST]: V stage landed and carries the ones column
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = warp_id(), lane = lane_id();
   const int nk = (p.Lk + BKV - 1) / BKV;
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_free[i], 4);
       mbar_init(&exp_tok[i], 4);
+      mbar_init(&v_ready[i], 1);
     }
     fence_barrier_init();
   }
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           for (int j = 0; j < nk; ++j, ++kc, ++vc) {
             mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
             if (lane == 0) mbar_arrive(&k_empty[kc % KST]);
-            mbar_wait(&v_full[vc % VST], (vc / VST) & 1);
+            mbar_wait(&v_ready[vc % VST], (vc / VST) & 1);
             if (lane == 0) mbar_arrive(&v_empty[vc % VST]);
             __syncwarp();
           }
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             // the unit's first PV overwrites O: the group must have read its previous O. Only
             // here -- the unit's first QK already ran during that epilogue
             if (j == 1 && un > 0) mbar_wait(&o_free[g], (un - 1) & 1);
-            mbar_wait(&v_full[vc % VST], (vc / VST) & 1);
+            mbar_wait(&v_ready[vc % VST], (vc / VST) & 1);
             mbar_wait(&p_full[g], pn & 1);
             tc_fence_after();
             if (elect_one()) {
@@ -383,6 +385,28 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         ++qc;
         ++un;
       }
+    } else if (warp == 2) {  // ----------------------------------- V fixup (row sums on the TC)
+      // head_dim 72 leaves V columns 72..79 of every stage zero (TMA out-of-bounds fill). Writing
+      // ones into column 72 makes the PV MMA produce O[:, 72] = sum_k P[:, k]: the softmax row sum
+      // comes out of the tensor core in fp32, from the same bf16 P as the numerator, and the
+      // softmax warps drop their per-element sum. Column 72 = element 8 of the 16-column SW32
+      // tail: 16 B chunk 1 of each 32 B row, swizzled with bit 2 of the row.
+      int vc = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int j = 0; j < nk; ++j, ++vc) {
+          const int vs = vc % VST;
+          mbar_wait(&v_full[vs], (vc / VST) & 1);
+          uint8_t* tail = sm + OFF_V + vs * (VA + VB) + VA;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = lane + 32 * i;
+            *reinterpret_cast<uint16_t*>(tail + r * 32 + (((r >> 2) & 1) ? 0 : 16)) = 0x3F80;  // bf16 1.0
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&v_ready[vs]);
+        }
+      }
     }
   } else {  // ------------------------------------------------------------ softmax groups
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
@@ -402,7 +426,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       decode(u, pr, head, seq, has1);
       if (g == 1 && !has1) continue;
       const int qt = 2 * pr + g;
-      float m = -INFINITY, l = 0.f;
+      float m = -INFINITY;
       for (int j = 0; j < nk; ++j, ++n) {
         mbar_wait(&s_full[g], n & 1);
         tc_fence_after();
@@ -441,7 +465,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         if (resc) {
           alpha = fast_exp2(m - m_new);
           m = m_new;
-          l *= alpha;
         }
         // MUFU turn: the two groups' exps phases alternate (g0 tile j, g1 tile j, g0 tile j+1, ...)
         // so each runs at the full SFU rate while the other does its max / P stores / waits,
@@ -450,9 +473,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         // exps first (packed bf16 P kept in the consumed s[] registers: chunk c -> s[4c..4c+3]),
         // so the MUFU work overlaps the tensor core finishing PV_{j-1}
         const float neg_m = -m;
-        float rs8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) rs8[e] = 0.f;
         if (full) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -470,7 +490,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
                 pv[e] = fast_exp2(x0);
                 pv[e + 1] = fast_exp2(x1);
               }
-              fadd2(rs8[e], rs8[e + 1], pv[e], pv[e + 1]);
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
@@ -484,7 +503,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
               for (int e = 0; e < 8; ++e) {
                 const int key = c * 8 + e;
                 pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
-                rs8[e] += pv[e];
               }
 #pragma unroll
               for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
@@ -525,7 +543,6 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         for (int c = 0; c < 16; ++c)  // chunk c (8 keys) -> region c / 8, 16 B swizzled
           st_shared_u4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), s[4 * c], s[4 * c + 1],
                        s[4 * c + 2], s[4 * c + 3]);
-        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
@@ -534,11 +551,12 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       // ---- unit epilogue: O / l -> bf16 -> staging (the P buffer, 144 B rows) -> TMA store
       mbar_wait(&pv_done[g], (n - 1) & 1);
       tc_fence_after();
-      uint32_t o[72];
+      uint32_t o[80];  // columns 0..71: O, column 72: the row sum l (ones column of V)
       tmem_ld32(o_tm, o);
       tmem_ld32(o_tm + 32, o + 32);
-      tmem_ld_32x32b_x8_fm(o_tm + 64, o + 64);
+      tmem_ld16(o_tm + 64, o + 64);
       tmem_ld_wait();
+      const float l = __uint_as_float(o[72]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[g]);
