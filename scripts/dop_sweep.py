@@ -29,6 +29,18 @@ from paper_2506_13497_b200.executor import exchange_bytes
 from paper_2506_13497_b200.stdit import STDiTModel, StepRequest, VirtualGroup
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+_peaks = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+PEAK_TFLOPS = (json.loads(_peaks.read_text())["bf16_tflops_sustained"] if _peaks.exists() else 1400.0)
+
+
+def step_flops(cfg, shape):
+    """Algorithmic FLOPs of one CFG step (the bench.py formula)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_bench", Path(__file__).resolve().parents[1] / "bench.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.step_flops(cfg, shape)
 
 
 def ev_time(fn, reps: int) -> float:
@@ -106,6 +118,12 @@ def main() -> None:
                 for r in grp.ranks:
                     r.close()
                 del grp, parts
+            # roofline: algorithmic FLOPs of the step (bench.step_flops) per GPU over the
+            # (projected) latency, against the measured sustained bf16 peak
+            fl = step_flops(cfg, sh)["total"]
+            row["step_tflop"] = round(fl / 1e12, 3)
+            row["tflops_per_gpu"] = round(fl / P / (row["projected_ms"] * 1e-3) / 1e12, 1)
+            row["frac_of_sustained_bf16"] = round(row["tflops_per_gpu"] / PEAK_TFLOPS, 3)
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
             row["wall_s"] = round(time.time() - t0, 1)
