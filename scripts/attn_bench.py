@@ -52,3 +52,14 @@ for tc in (False, True):
     t = timeit(lambda: kernels.attention(qkv2[:, :C], qkv2[:, C:2 * C], qkv2[:, 2 * C:], o2, heads=H, num_seqs=B * T2,
                                          Lq=S2, Lk=S2, q_map=(1, S2, 0, 1), kv_map=(1, S2, 0, 1), tc=tc), it=5)
     print(f"spatial720 tc={tc}: {t:7.1f} us  {fl2 / t / 1e6:6.1f} TF/s", flush=True)
+# temporal attention in the long-clip regime (480p/720p x 102 frames: T = 30)
+for (T3, S3) in ((30, 1620), (30, 3600)):
+    M3 = B * T3 * S3
+    qkv3 = torch.randn(M3, 3 * C, device=dev).bfloat16()
+    o3 = torch.empty(M3, C, device=dev, dtype=torch.bfloat16)
+    mp3 = (S3, T3 * S3, 1, S3)
+    t = timeit(lambda: kernels.attention(qkv3[:, :C], qkv3[:, C:2 * C], qkv3[:, 2 * C:], o3, heads=H,
+                                         num_seqs=B * S3, Lq=T3, Lk=T3, q_map=mp3, kv_map=mp3, temporal=True), it=5)
+    print(f"temporal T={T3} S={S3}: {t:7.1f} us  {M3 * 4 * C * 2 / t / 1e3:6.1f} GB/s "
+          f"{4 * B * S3 * T3 * T3 * C / t / 1e6:6.1f} TF/s", flush=True)
+    del qkv3, o3
