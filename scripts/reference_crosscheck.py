@@ -7,7 +7,8 @@ reference ``ditsim`` (read-only import from /root/reference/pkg/src) -- load_pro
 derive_dop_table, generate, Simulation + GreedyPolicy, compute_metrics -- for the same config-5
 workload, and records the reference's predicted avg / p99 latency and GPU-seconds next to this
 repo's own prediction (sched, bit-exact re-implementation) and the replay that executed every
-step on the GPU. Output: profiles/r01_reference_crosscheck.json (read by
+step on the GPU, plus the reference's occupancy lower bound (optimal.solve_optimal) for the
+cost-over-optimum. Output: profiles/r01_reference_crosscheck.json (read by
 tests/test_sched_golden.py::test_reference_crosscheck_of_b200_profile).
 """
 from __future__ import annotations
@@ -43,6 +44,24 @@ def main() -> None:
             "b200_replayed": run["replayed"].get(rate),
         }
         print(rate, out["rates"][rate], flush=True)
+    # the reference's occupancy lower bound for the same mix (optimal.solve_optimal with the batch
+    # model, as its experiment harness computes it, experiment.py:289-308) -> cost over optimum of
+    # the greedy trace on the B200-measured profile
+    from ditsim.optimal import BatchModel, InfeasibleError, solve_optimal
+
+    try:
+        opt = solve_optimal(ds.ClusterTopology(1, 8), table, mix, BatchModel(run["requests"]),
+                            steps=run["denoise_steps"], include_vae=True)
+        out["optimal_gpu_seconds"] = round(opt.total_gpu_seconds, 3)
+        for rec in out["rates"].values():
+            rec["reference"]["cost_over_optimum"] = round(rec["reference"]["gpu_seconds"] / opt.total_gpu_seconds, 4)
+            if rec.get("b200_replayed"):
+                rec["b200_replayed_cost_over_optimum"] = round(
+                    rec["b200_replayed"]["gpu_seconds"] / opt.total_gpu_seconds, 4)
+    except InfeasibleError as e:  # pragma: no cover
+        out["optimal_gpu_seconds"] = None
+        out["optimal_error"] = str(e)
+    print("optimal GPU-seconds:", out.get("optimal_gpu_seconds"), flush=True)
     (ROOT / "profiles" / "r01_reference_crosscheck.json").write_text(json.dumps(out, indent=1))
 
 
