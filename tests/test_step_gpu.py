@@ -153,3 +153,27 @@ def test_graph_replay_matches_eager(cuda):
         req.graph_step(z2, step)
     torch.cuda.synchronize()
     assert torch.equal(z1, z2)
+
+
+def test_tiny_full_trajectory_matches_oracle(cuda):
+    """All 30 RFLOW steps (the whole denoising trajectory) of the tiny config on the GPU vs the
+    fp32 CPU oracle from the same z0: bf16 errors must not compound over the trajectory."""
+    from oracle import stdit3
+    from paper_2506_13497_b200 import weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W, sh, z, y = _setup(cfg, "144p-16f")
+    text = stdit3.prepare_text(W, y)
+    model = STDiTModel(cfg, W, cuda)
+    req = StepRequest(model, sh, y.to(cuda))
+    zd = z.to(cuda).contiguous()
+    zr = z.clone()
+    errs = []
+    for step in range(30):
+        req.step(zd, step)
+        zr = stdit3.denoise_step(W, cfg, zr, text, step, sh.height, sh.width)
+        torch.cuda.synchronize()
+        errs.append(rel_l2(zd.cpu(), zr))
+    print("trajectory relL2 every 5 steps:", [f"{e:.1e}" for e in errs[::5]], f"final {errs[-1]:.2e}")
+    assert max(errs) <= 2e-2
