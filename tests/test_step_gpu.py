@@ -177,3 +177,17 @@ def test_tiny_full_trajectory_matches_oracle(cuda):
         errs.append(rel_l2(zd.cpu(), zr))
     print("trajectory relL2 every 5 steps:", [f"{e:.1e}" for e in errs[::5]], f"final {errs[-1]:.2e}")
     assert max(errs) <= 2e-2
+
+
+def test_xl2_full_depth_step_matches_oracle(cuda):
+    """The real model (STDiT3-XL/2, all 28 block pairs, C = 1152) at a real shape (144p x 51:
+    latent 15x18x32, 2160 tokens per sample) against the fp32 oracle, one step."""
+    from paper_2506_13497_b200 import weights
+
+    cfg = weights.XL2
+    W, sh, z, y = _setup(cfg, "144p")
+    ref = _oracle(cfg, W, sh, z, y, 11)
+    out = _gpu(cfg, W, sh, z, y, 11, cuda)
+    e_z, e_v = rel_l2(out, ref), rel_l2(out - z, ref - z)
+    print(f"xl2 full depth 144p: relL2 z'={e_z:.2e} update={e_v:.2e}")
+    assert e_z <= 1e-2 and e_v <= 2e-2
