@@ -191,3 +191,29 @@ def test_xl2_full_depth_step_matches_oracle(cuda):
     e_z, e_v = rel_l2(out, ref), rel_l2(out - z, ref - z)
     print(f"xl2 full depth 144p: relL2 z'={e_z:.2e} update={e_v:.2e}")
     assert e_z <= 1e-2 and e_v <= 2e-2
+
+
+def test_rebound_and_broadcast_text_state_match_fresh_requests(cuda):
+    """ddit_request_set_text (re-binding a pooled rank state to a new caption) and
+    ddit_request_copy_text (the promotion broadcast) give exactly the step of a freshly opened
+    request with that caption."""
+    from paper_2506_13497_b200 import weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=2)
+    W, sh, z, y = _setup(cfg, "144p-16f")
+    _, y2 = weights.synthetic_inputs(cfg, sh.latent, seed_z=7, seed_y=8)
+    model = STDiTModel(cfg, W, cuda)
+    fresh = StepRequest(model, sh, y2.to(cuda))
+    z_ref = z.to(cuda).contiguous()
+    fresh.step(z_ref, 4)
+    pooled = StepRequest(model, sh, y.to(cuda))  # opened for another caption
+    pooled.set_text(y2.to(cuda))
+    z_a = z.to(cuda).contiguous()
+    pooled.step(z_a, 4)
+    other = StepRequest(model, sh, y.to(cuda))
+    other.copy_text_from(fresh)
+    z_b = z.to(cuda).contiguous()
+    other.step(z_b, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(z_a, z_ref) and torch.equal(z_b, z_ref)
