@@ -217,3 +217,23 @@ def test_rebound_and_broadcast_text_state_match_fresh_requests(cuda):
     other.step(z_b, 4)
     torch.cuda.synchronize()
     assert torch.equal(z_a, z_ref) and torch.equal(z_b, z_ref)
+
+
+@pytest.mark.parametrize("dop", [4, 8])
+def test_virtual_dop_long_clip_matches_dop1(cuda, dop):
+    """BASELINE config 3's long-clip shape (720p x 102: T = 30, S = 3600 tokens per frame) at
+    DoP 4 / 8 (virtual ranks, fused exchange) reproduces DoP 1 bit for bit (reduced width)."""
+    from paper_2506_13497_b200 import weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest, VirtualGroup
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W, sh, z, y = _setup(cfg, "720p-102f")
+    model = STDiTModel(cfg, W, cuda)
+    yd = y.to(cuda)
+    z1 = z.to(cuda).contiguous()
+    StepRequest(model, sh, yd).step(z1, 9)
+    grp = VirtualGroup(model, sh, yd, dop)
+    parts = grp.split(z.to(cuda))
+    grp.step(parts, 9)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, dim=2), z1)
