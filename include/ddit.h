@@ -258,7 +258,8 @@ DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream);
 
 /* GroupNorm over channels-last x [N][P][C] bf16 (per sample n, group of C/G channels, all P
  * pixels), affine, optional SiLU -> y bf16. Deterministic (fixed reduction order).
- * stats: device scratch of at least N*G*2 doubles + N*512*G float2. */
+ * stats: device scratch of at least N*G*2 doubles + N*512*G float2 (partials) + N*C float2
+ * (per-channel affine coefficients). */
 DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
                             const float* beta, int N, int P, int C, int G, float eps, int silu_act,
                             void* stream);
@@ -268,12 +269,16 @@ DDIT_API int ddit_upsample2x(const void* x, void* y, int N, int H, int W, int C,
 DDIT_API int ddit_depth_to_time(const void* x, void* y, int B, int T, int HW, int C, void* stream);
 /* Direct conv (CUDA cores) for layers with < 64 channels on one side. x strided
  * (x_strides = element strides {b, c, t, h, w}, NULL = dense channels-last), bf16 or fp32;
- * w fp32 [Cout][kt][kh][kw][Cin]; y bf16 channels-last, or fp32 [B][Cout][T][Hc][Wc] cropped
+ * w fp32 [kt][kh][kw][Cin][Cout]; y bf16 channels-last, or fp32 [B][Cout][T][Hc][Wc] cropped
  * when out_cf. */
 DDIT_API int ddit_conv_small(const void* x, int x_is_f32, const long long* x_strides,
                              const float* w, const float* bias, void* y, int B, int T, int H, int W,
                              int Cin, int Cout, int kt, int kh, int kw, int causal_time, int out_cf,
                              int Hc, int Wc, void* stream);
+/* decoded frames: channels [0, C) of bf16 channels-last y [N][H][W][ld] -> fp32 [C][N][Hc][Wc]
+ * (the video tensor [1][C][N][Hc][Wc], cropped to Hc x Wc) */
+DDIT_API int ddit_frames_out(const void* y, float* out, int N, int H, int W, int ld, int C, int Hc,
+                             int Wc, void* stream);
 /* mid-block attention helpers: row softmax (fp32 S -> bf16 P, columns >= valid -> 0),
  * bf16 transpose with zero-padded output rows, y = bf16(a_f32 + b_bf16) */
 DDIT_API int ddit_softmax_rows(const float* S, void* P, int rows, int cols, int valid, float scale,

@@ -154,6 +154,7 @@ _SIGNATURES = {
     "ddit_groupnorm": [vp, vp, vp, vp, vp, ci, ci, ci, ci, cf, ci, vp],
     "ddit_upsample2x": [vp, vp, ci, ci, ci, ci, vp],
     "ddit_depth_to_time": [vp, vp, ci, ci, ci, ci, vp],
+    "ddit_frames_out": [vp, vp, ci, ci, ci, ci, ci, ci, ci, vp],
     "ddit_conv_small": [vp, ci, vp, vp, vp, vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, vp],
     "ddit_softmax_rows": [vp, vp, ci, ci, ci, cf, vp],
     "ddit_transpose_bf16": [vp, vp, ci, ci, ci, ci, vp],

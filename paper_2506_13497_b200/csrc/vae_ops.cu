@@ -12,10 +12,20 @@
 namespace ddit {
 
 // ------------------------------------------------------------------ GroupNorm
-// Deterministic two-level statistics (fixed reduction order: bitwise reproducible).
-// gn_partial: block (blk, n) reduces pixels [blk*ppb, (blk+1)*ppb) of sample n into
-// partial[n][blk][g] = (sum, sumsq); thread t owns the 8-channel vector t % (C/8) (C/8 divides
-// 256) and walks pixels with stride 256 / (C/8).
+// Deterministic two-level statistics (fixed reduction order: bitwise reproducible), then one
+// streaming pass:
+//   gn_partial:  block (blk, n) reduces pixels [blk*ppb, (blk+1)*ppb) of sample n into
+//                partial[n][blk][g] = (sum, sumsq). Thread t owns the 8-channel vector t % (C/8)
+//                (C/8 divides 256), walks pixels with stride 256 / (C/8), 4 loads in flight, folds
+//                its 8 channels into their group(s) and the G owner threads add the 256/G
+//                contributions of their group in a fixed order.
+//   gn_finalize: fp64 sum of the partials in block order -> mean / rstd per (n, g) -> per-channel
+//                affine coefficients coef[n][c] = (a, b), a = rstd*gamma, b = beta - mean*a.
+//   gn_apply:    y = act(x*a + b), one FMA per element (+ SiLU as x*(0.5 + 0.5*tanh(x/2)), one MUFU
+//                op); the thread's channel vector is fixed, so its 16 coefficients stay in registers.
+constexpr int kGnUnroll = 4;       // vectors in flight per thread, apply
+constexpr int kGnPartUnroll = 8;   // and statistics
+
 __global__ void __launch_bounds__(256)
     gn_partial_kernel(const __nv_bfloat16* __restrict__ x, float2* __restrict__ partial, int P,
                       int C, int G, int ppb, int nblk) {
@@ -26,94 +36,150 @@ __global__ void __launch_bounds__(256)
   const int v = threadIdx.x % vecs;
   const int p0 = blk * ppb;
   const int p1 = min(p0 + ppb, P);
-  __shared__ float red_s[256][9], red_q[256][9];
+  __shared__ float2 red[256][8];
   float sg[8], qg[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) sg[e] = qg[e] = 0.f;
-  for (int p = p0 + (int)threadIdx.x / vecs; p < p1; p += step) {
-    const uint4 u = *reinterpret_cast<const uint4*>(x + ((size_t)n * P + p) * C + v * 8);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  const __nv_bfloat16* base = x + (size_t)n * P * C + v * 8;
+  for (int p = p0 + (int)threadIdx.x / vecs; p < p1; p += kGnPartUnroll * step) {
+    uint4 u[kGnPartUnroll];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = unpack_bf16(w[e]);
-      sg[2 * e] += f.x;
-      sg[2 * e + 1] += f.y;
-      qg[2 * e] += f.x * f.x;
-      qg[2 * e + 1] += f.y * f.y;
+    for (int k = 0; k < kGnPartUnroll; ++k)
+      u[k] = (p + k * step < p1) ? __ldcs(reinterpret_cast<const uint4*>(base + (size_t)(p + k * step) * C))
+                                 : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kGnPartUnroll; ++k) {
+      const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = unpack_bf16(w[e]);
+        sg[2 * e] += f.x;
+        sg[2 * e + 1] += f.y;
+        qg[2 * e] = fmaf(f.x, f.x, qg[2 * e]);
+        qg[2 * e + 1] = fmaf(f.y, f.y, qg[2 * e + 1]);
+      }
     }
   }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    red_s[threadIdx.x][e] = sg[e];
-    red_q[threadIdx.x][e] = qg[e];
+  // fold the 8 channels into their group(s): slot j holds group (v*8 + j*cg) / cg
+  const int gpv = cg >= 8 ? 1 : 8 / cg;  // groups per 8-channel vector
+  const int width = 8 / gpv;
+  for (int j = 0; j < gpv; ++j) {
+    float s = 0.f, q = 0.f;
+    for (int e = j * width; e < (j + 1) * width; ++e) {
+      s += sg[e];
+      q += qg[e];
+    }
+    red[threadIdx.x][j] = make_float2(s, q);
   }
   __syncthreads();
   if (threadIdx.x < G) {
     const int g = threadIdx.x;
     float s = 0.f, q = 0.f;
-    for (int t = 0; t < 256; ++t) {
-      const int c0 = (t % vecs) * 8;
-      if (c0 + 8 <= g * cg || c0 >= (g + 1) * cg) continue;
-      for (int e = 0; e < 8; ++e)
-        if ((c0 + e) / cg == g) {
-          s += red_s[t][e];
-          q += red_q[t][e];
+    if (cg >= 8) {
+      const int vpg = cg / 8;
+      for (int k = 0; k < step; ++k)
+        for (int j = 0; j < vpg; ++j) {
+          const float2 r = red[k * vecs + g * vpg + j][0];
+          s += r.x;
+          q += r.y;
         }
+    } else {
+      for (int k = 0; k < step; ++k) {
+        const float2 r = red[k * vecs + g / gpv][g % gpv];
+        s += r.x;
+        q += r.y;
+      }
     }
     partial[((size_t)n * nblk + blk) * G + g] = make_float2(s, q);
   }
 }
 
-__global__ void gn_finalize_kernel(const float2* __restrict__ partial, double* __restrict__ stats,
-                                   int G, int nblk) {
-  const int n = blockIdx.x, g = threadIdx.x;
-  if (g >= G) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; ++b) {
-    const float2 v = partial[((size_t)n * nblk + b) * G + g];
-    s += v.x;
-    q += v.y;
+__global__ void __launch_bounds__(256)
+    gn_finalize_kernel(const float2* __restrict__ partial, float2* __restrict__ coef,
+                       const float* __restrict__ gamma, const float* __restrict__ beta, int P,
+                       int C, int G, int nblk, float eps) {
+  const int n = blockIdx.x;
+  __shared__ double mean_s[32], rstd_s[32];
+  // one warp per group: lanes take blocks lane, lane+32, ... then a fixed xor tree (deterministic)
+  const int lane = threadIdx.x & 31;
+  for (int g = threadIdx.x >> 5; g < G; g += blockDim.x >> 5) {
+    double s = 0, q = 0;
+    for (int b = lane; b < nblk; b += 32) {
+      const float2 v = partial[((size_t)n * nblk + b) * G + g];
+      s += v.x;
+      q += v.y;
+    }
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if (lane == 0) {
+      const double cnt = (double)P * (C / G);
+      const double mean = s / cnt;
+      const double var = fmax(q / cnt - mean * mean, 0.0);
+      mean_s[g] = mean;
+      rstd_s[g] = (double)rsqrtf((float)var + eps);
+    }
   }
-  stats[(n * G + g) * 2] = s;
-  stats[(n * G + g) * 2 + 1] = q;
+  __syncthreads();
+  const int cg = C / G;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double a = rstd_s[c / cg] * (double)gamma[c];
+    coef[(size_t)n * C + c] = make_float2((float)a, (float)((double)beta[c] - mean_s[c / cg] * a));
+  }
 }
 
-// y = act((x - mean) * rstd * gamma + beta), act = SiLU or identity; bf16 in / out.
+DDIT_DEV float silu_fast(float v) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
+  return v * fmaf(0.5f, t, 0.5f);
+}
+
+// grid (chunks, N); block chunk covers 256*kGnUnroll consecutive 8-channel vectors of sample n
+template <bool SILU>
 __global__ void __launch_bounds__(256)
     gn_apply_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                    const double* __restrict__ stats, const float* __restrict__ gamma,
-                    const float* __restrict__ beta, int P, int C, int G, float eps, int silu_act,
-                    size_t total_vecs) {
-  const int cg = C / G;
+                    const float2* __restrict__ coef, int C, size_t vecs_per_n) {
+  const int n = blockIdx.y;
   const int vecs = C / 8;
-  const double cnt = (double)P * cg;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total_vecs;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t pix = i / vecs;
-    const int c0 = (int)(i % vecs) * 8;
-    const int n = (int)(pix / P);
-    const uint4 u = reinterpret_cast<const uint4*>(x)[i];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  const int v = threadIdx.x % vecs;  // fixed: 256 is a multiple of C/8
+  float a[8], b[8];
+  {
+    const float4* cp = reinterpret_cast<const float4*>(coef + (size_t)n * C + v * 8);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 f = cp[k];
+      a[2 * k] = f.x;
+      b[2 * k] = f.y;
+      a[2 * k + 1] = f.z;
+      b[2 * k + 1] = f.w;
+    }
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(x) + (size_t)n * vecs_per_n;
+  uint4* dst = reinterpret_cast<uint4*>(y) + (size_t)n * vecs_per_n;
+  const size_t i0 = (size_t)blockIdx.x * 256 * kGnUnroll + threadIdx.x;
+  uint4 u[kGnUnroll];
+#pragma unroll
+  for (int k = 0; k < kGnUnroll; ++k) {
+    const size_t i = i0 + (size_t)k * 256;
+    u[k] = i < vecs_per_n ? __ldcs(src + i) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kGnUnroll; ++k) {
+    const size_t i = i0 + (size_t)k * 256;
+    const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
     uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = unpack_bf16(w[e]);
-      float r[2] = {f.x, f.y};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = c0 + 2 * e + h;
-        const int g = c / cg;
-        const double s = stats[(n * G + g) * 2], q = stats[(n * G + g) * 2 + 1];
-        const double mean = s / cnt;
-        const double var = fmax(q / cnt - mean * mean, 0.0);
-        const float rstd = rsqrtf((float)var + eps);
-        float v = (r[h] - (float)mean) * rstd * gamma[c] + beta[c];
-        if (silu_act) v = v / (1.f + __expf(-v));
-        r[h] = v;
+      float r0 = fmaf(f.x, a[2 * e], b[2 * e]), r1 = fmaf(f.y, a[2 * e + 1], b[2 * e + 1]);
+      if (SILU) {
+        r0 = silu_fast(r0);
+        r1 = silu_fast(r1);
       }
-      o[e] = pack_bf16(r[0], r[1]);
+      o[e] = pack_bf16(r0, r1);
     }
-    reinterpret_cast<uint4*>(y)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    if (i < vecs_per_n) dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -155,50 +221,108 @@ __global__ void depth_to_time_kernel(const __nv_bfloat16* __restrict__ x,
 
 // ------------------------------------------------------------------ small-channel conv
 // Direct conv for layers with < 64 channels on one side. x: any strided 5-D layout
-// (element strides xs = {b, c, t, h, w}; bf16 or fp32), w: fp32 [Cout][kt][kh][kw][Cin],
-// y: [B][T][H][W][Cout] bf16, or fp32 channels-first [B][Cout][T][Hc][Wc] cropped to (Hc, Wc)
-// when out_cf is set (the decoded frames).
+// (element strides xs = {b, c, t, h, w}; bf16 or fp32), w: fp32 [kt][kh][kw][Cin][Cout] (lanes
+// read consecutive output channels), y: [B][T][H][W][Cout] bf16, or fp32 channels-first
+// [B][Cout][T][Hc][Wc] cropped to (Hc, Wc) when out_cf is set. A warp computes kConvSmallPix
+// consecutive pixels, lanes over output channels: each weight load feeds kConvSmallPix FMAs,
+// the input loads are warp broadcasts.
 struct XStrides {
   long long b, c, t, h, w;
 };
-template <typename TIn>
+constexpr int kConvSmallPix = 4;
+// COL output channels per lane (lane, lane+32, ...): the tap's input values, loaded once, feed
+// kConvSmallPix x COL FMAs
+template <typename TIn, int COL>
 __global__ void __launch_bounds__(128)
     conv_small_kernel(const TIn* __restrict__ x, XStrides xs, const float* __restrict__ w,
                       const float* __restrict__ bias, void* __restrict__ y, int B, int T, int H,
                       int W, int Cin, int Cout, int kt, int kh, int kw, int pt, int out_cf, int Hc,
                       int Wc) {
-  const size_t pix = blockIdx.x * (size_t)blockDim.y + threadIdx.y;
+  constexpr int NP = kConvSmallPix;
   const size_t npix = (size_t)B * T * H * W;
-  if (pix >= npix) return;
-  const int xq = (int)(pix % W);
-  size_t r = pix / W;
-  const int yq = (int)(r % H);
-  r /= H;
-  const int tq = (int)(r % T);
-  const int b = (int)(r / T);
-  for (int co = threadIdx.x; co < Cout; co += blockDim.x) {
-    float acc = bias ? bias[co] : 0.f;
-    for (int dt = 0; dt < kt; ++dt) {
-      const int ti = tq + dt - pt;
-      if (ti < 0 || ti >= T) continue;
-      for (int dy = 0; dy < kh; ++dy) {
-        const int yi = yq + dy - kh / 2;
-        if (yi < 0 || yi >= H) continue;
+  const size_t pix0 = ((size_t)blockIdx.x * blockDim.y + threadIdx.y) * NP;
+  if (pix0 >= npix) return;
+  int bq[NP], tq[NP], yq[NP], xq[NP];
+  bool ok[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const size_t pix = pix0 + p;
+    ok[p] = pix < npix;
+    const size_t q = ok[p] ? pix : pix0;
+    xq[p] = (int)(q % W);
+    size_t r = q / W;
+    yq[p] = (int)(r % H);
+    r /= H;
+    tq[p] = (int)(r % T);
+    bq[p] = (int)(r / T);
+  }
+  for (int co0 = threadIdx.x; co0 < Cout; co0 += 32 * COL) {
+    float acc[NP][COL];
+#pragma unroll
+    for (int j = 0; j < COL; ++j) {
+      const int co = co0 + 32 * j;
+      const float b0 = (bias && co < Cout) ? bias[co] : 0.f;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) acc[p][j] = b0;
+    }
+    for (int dt = 0; dt < kt; ++dt)
+      for (int dy = 0; dy < kh; ++dy)
         for (int dx = 0; dx < kw; ++dx) {
-          const int xi = xq + dx - kw / 2;
-          if (xi < 0 || xi >= W) continue;
-          const TIn* xp = x + b * xs.b + ti * xs.t + yi * xs.h + xi * xs.w;
-          const float* wp = w + ((((size_t)co * kt + dt) * kh + dy) * kw + dx) * Cin;
-          for (int ci = 0; ci < Cin; ++ci) acc += wp[ci] * static_cast<float>(xp[ci * xs.c]);
+          const TIn* xp[NP];
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const int ti = tq[p] + dt - pt, yi = yq[p] + dy - kh / 2, xi = xq[p] + dx - kw / 2;
+            xp[p] = (ti < 0 || ti >= T || yi < 0 || yi >= H || xi < 0 || xi >= W)
+                        ? nullptr
+                        : x + bq[p] * xs.b + ti * xs.t + yi * xs.h + xi * xs.w;
+          }
+          const float* wp = w + (((size_t)dt * kh + dy) * kw + dx) * Cin * Cout + co0;
+          for (int ci = 0; ci < Cin; ++ci) {
+            float xv[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) xv[p] = xp[p] ? static_cast<float>(xp[p][ci * xs.c]) : 0.f;
+#pragma unroll
+            for (int j = 0; j < COL; ++j) {
+              const float wv = (co0 + 32 * j < Cout) ? wp[(size_t)ci * Cout + 32 * j] : 0.f;
+#pragma unroll
+              for (int p = 0; p < NP; ++p) acc[p][j] = fmaf(wv, xv[p], acc[p][j]);
+            }
+          }
+        }
+#pragma unroll
+    for (int j = 0; j < COL; ++j) {
+      const int co = co0 + 32 * j;
+      if (co >= Cout) continue;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        if (!ok[p]) continue;
+        if (out_cf) {
+          if (yq[p] < Hc && xq[p] < Wc)
+            static_cast<float*>(y)[((((size_t)bq[p] * Cout + co) * T + tq[p]) * Hc + yq[p]) * Wc + xq[p]] =
+                acc[p][j];
+        } else {
+          static_cast<__nv_bfloat16*>(y)[(pix0 + p) * Cout + co] = __float2bfloat16(acc[p][j]);
         }
       }
     }
-    if (out_cf) {
-      if (yq < Hc && xq < Wc)
-        static_cast<float*>(y)[((((size_t)b * Cout + co) * T + tq) * Hc + yq) * Wc + xq] = acc;
-    } else {
-      static_cast<__nv_bfloat16*>(y)[pix * Cout + co] = __float2bfloat16(acc);
-    }
+  }
+}
+
+// decoded frames: channels 0..C-1 of bf16 channels-last y [N][H][W][ld] -> fp32 channels-first
+// [C][N][Hc][Wc] (the video tensor [1][C][N][Hc][Wc], cropped); one thread per output pixel, the
+// C stores coalesced across threads
+__global__ void __launch_bounds__(256)
+    frames_out_kernel(const __nv_bfloat16* __restrict__ y, float* __restrict__ out, int N, int H,
+                      int W, int ld, int C, int Hc, int Wc) {
+  const size_t plane = (size_t)Hc * Wc;
+  const size_t total = (size_t)N * plane;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / plane);
+    const int r = (int)(i % plane);
+    const int yy = r / Wc, xx = r % Wc;
+    const __nv_bfloat16* src = y + (((size_t)n * H + yy) * W + xx) * ld;
+    for (int c = 0; c < C; ++c) out[((size_t)c * N + n) * plane + r] = __bfloat162float(src[c]);
   }
 }
 
@@ -285,20 +409,29 @@ DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* 
     set_error("groupnorm: C a power of two in [8, 2048] divisible by G <= 32 required");
     return DDIT_E_INVALID;
   }
-  int ppb = 1024;
-  int nblk = (P + ppb - 1) / ppb;
-  if (nblk > 512) {  // bound the partial buffer: larger pixel chunks per block
-    ppb = (P + 511) / 512;
-    nblk = (P + ppb - 1) / ppb;
-  }
+  // >= 1024 pixels per block, but >= 2 blocks per SM of one sample (temporal-VAE calls have
+  // N = 1); at most 512 blocks per sample (partial buffer bound). The partition depends on P and C
+  // only, never on N: a frame's statistics must not change with how many frames share the call
+  // (VAE DoP decodes frame ranges and must reproduce the whole decode bit for bit).
+  const int step = 256 / (C / 8);
+  int nblk = (P + 1023) / 1024;
+  nblk = std::max(nblk, std::min(296, (P + step * kGnPartUnroll - 1) / (step * kGnPartUnroll)));
+  nblk = std::max(1, std::min(nblk, 512));
+  const int ppb = (P + nblk - 1) / nblk;
+  nblk = (P + ppb - 1) / ppb;
   float2* partial = reinterpret_cast<float2*>(stats + (size_t)N * G * 2);
+  float2* coef = partial + (size_t)N * nblk * G;
   gn_partial_kernel<<<dim3(nblk, N), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), partial, P,
                                                   C, G, ppb, nblk);
-  gn_finalize_kernel<<<N, 32, 0, s>>>(partial, stats, G, nblk);
-  const size_t vecs = (size_t)N * P * (C / 8);
-  gn_apply_kernel<<<blocks_for(vecs, 256), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
-                                                         static_cast<__nv_bfloat16*>(y), stats,
-                                                         gamma, beta, P, C, G, eps, silu_act, vecs);
+  gn_finalize_kernel<<<N, 256, 0, s>>>(partial, coef, gamma, beta, P, C, G, nblk, eps);
+  const size_t vpn = (size_t)P * (C / 8);
+  const dim3 grid((unsigned)((vpn + 256 * kGnUnroll - 1) / (256 * kGnUnroll)), N);
+  if (silu_act)
+    gn_apply_kernel<true><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                               static_cast<__nv_bfloat16*>(y), coef, C, vpn);
+  else
+    gn_apply_kernel<false><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                static_cast<__nv_bfloat16*>(y), coef, C, vpn);
   return check_cuda("groupnorm");
 }
 
@@ -335,16 +468,30 @@ DDIT_API int ddit_conv_small(const void* x, int x_is_f32, const long long* x_str
   const size_t npix = (size_t)B * T * H * W;
   dim3 block(32, 4);
   const int pt = causal_time ? kt - 1 : kt / 2;
-  const int grid = (int)((npix + 3) / 4);
+  const int grid = (int)((npix + 4 * kConvSmallPix - 1) / (4 * kConvSmallPix));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (x_is_f32)
-    conv_small_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(x), xs, w, bias, y, B,
-                                                   T, H, W, Cin, Cout, kt, kh, kw, pt, out_cf, Hc, Wc);
-  else
-    conv_small_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(x), xs, w, bias, y, B, T, H, W, Cin, Cout, kt, kh, kw, pt,
-        out_cf, Hc, Wc);
+  const bool wide = Cout % 128 == 0;
+#define DDIT_CONV_SMALL(TIN, COL)                                                              \
+  conv_small_kernel<TIN, COL><<<grid, block, 0, s>>>(static_cast<const TIN*>(x), xs, w, bias, y, B, \
+                                                     T, H, W, Cin, Cout, kt, kh, kw, pt, out_cf, Hc, Wc)
+  if (x_is_f32) {
+    if (wide) DDIT_CONV_SMALL(float, 4); else DDIT_CONV_SMALL(float, 1);
+  } else {
+    if (wide) DDIT_CONV_SMALL(__nv_bfloat16, 4); else DDIT_CONV_SMALL(__nv_bfloat16, 1);
+  }
+#undef DDIT_CONV_SMALL
   return check_cuda("conv_small");
+}
+
+DDIT_API int ddit_frames_out(const void* y, float* out, int N, int H, int W, int ld, int C, int Hc,
+                             int Wc, void* stream) {
+  if (C > ld || Hc > H || Wc > W) {
+    set_error("frames_out: crop larger than the source");
+    return DDIT_E_INVALID;
+  }
+  frames_out_kernel<<<blocks_for((size_t)N * Hc * Wc, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(y), out, N, H, W, ld, C, Hc, Wc);
+  return check_cuda("frames_out");
 }
 
 DDIT_API int ddit_softmax_rows(const float* S, void* P, int rows, int cols, int valid, float scale,

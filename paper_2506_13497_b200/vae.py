@@ -31,11 +31,22 @@ def _bf16(t):
     return t.to(torch.bfloat16).contiguous()
 
 
+def _small(w: torch.Tensor) -> torch.Tensor:
+    """fp32 [Cout][kt][kh][kw][Cin] -> [kt][kh][kw][Cin][Cout] (ddit_conv_small's layout)."""
+    return w.float().permute(1, 2, 3, 4, 0).contiguous()
+
+
 class VAEDecoder:
     """OpenSora-1.2 VAE decoder with device-resident weights on one GPU."""
 
-    def __init__(self, cfg: VAEConfig, weights: dict[str, torch.Tensor], device="cuda:0"):
+    def __init__(self, cfg: VAEConfig, weights: dict[str, torch.Tensor], device="cuda:0",
+                 graphs: int = 0):
+        """``graphs``: how many decode shapes keep a captured CUDA graph (0 = always eager). Off
+        by default: a graph's private pool keeps every activation of the decode resident (720p:
+        ~150 GB) for ~3 % at 240p, where the kernels already hide the launch overhead."""
         self.cfg = cfg
+        self.max_graphs = graphs
+        self._graphs: dict = {}
         self.dev = torch.device(device)
         d = self.dev
         W = {k: v.to(d) for k, v in weights.items()}
@@ -44,10 +55,12 @@ class VAEDecoder:
         sc = torch.tensor(cfg.scale, device=d)
         sh = torch.tensor(cfg.shift, device=d)
         wq = W["t.post_quant_conv.weight"]  # [4, 1, 1, 1, 4]
-        self.t_pq_w = (wq * sc.view(1, 1, 1, 1, -1)).contiguous()
+        self.t_pq_w = _small(wq * sc.view(1, 1, 1, 1, -1))
         self.t_pq_b = (W["t.post_quant_conv.bias"] + (wq[:, 0, 0, 0, :] * sh).sum(-1)).contiguous()
         # fold 1 / scaling_factor into the spatial post_quant_conv (1x1: exact)
-        self.s_pq_w = (W["s.post_quant_conv.weight"] / cfg.scaling_factor).contiguous()
+        self.s_pq_w = _small(W["s.post_quant_conv.weight"] / cfg.scaling_factor)
+        # direct (CUDA-core) convs take fp32 weights [kt][kh][kw][Cin][Cout]
+        self.small = {k: _small(W[k]) for k in ("t.conv1.weight", "s.conv_in.weight")}
         self.s_pq_b = W["s.post_quant_conv.bias"].contiguous()
         self.bf: dict[str, torch.Tensor] = {}
         for k, v in list(W.items()):
@@ -68,8 +81,9 @@ class VAEDecoder:
         self.w_qkv = _bf16(torch.cat([W[a + "to_q.weight"], W[a + "to_k.weight"], W[a + "to_v.weight"]]))
         self.b_qkv = torch.cat([W[a + "to_q.bias"], W[a + "to_k.bias"], W[a + "to_v.bias"]]).contiguous()
         self.w_out = _bf16(W[a + "to_out.weight"])
-        # GroupNorm scratch: fp64 [N][G][2] + fp32x2 partials [N][512][G], N <= 256 samples
-        self.stats = torch.empty(256 * 32 * 2 + 256 * 512 * 32, dtype=torch.float64, device=d)
+        # GroupNorm scratch: fp64 [N][G][2] + fp32x2 partials [N][512][G] + fp32x2 coefficients
+        # [N][C], N <= 256 samples, C <= 2048
+        self.stats = torch.empty(256 * 32 * 2 + 256 * 512 * 32 + 256 * 2048, dtype=torch.float64, device=d)
         self.launches = 0
 
     # ---------------------------------------------------------------- primitives
@@ -89,13 +103,13 @@ class VAEDecoder:
     def _conv_small(self, x, w, b, *, out_shape, causal=True, x_f32=False, strides=None,
                     out_cf=False, crop=(0, 0)):
         B, T, H, Wd, Cout = out_shape
-        Cout_w, kt, kh, kw, Cin = w.shape
+        kt, kh, kw, Cin, Cout_w = w.shape
         if out_cf:
             y = torch.empty((B, Cout, T, crop[0], crop[1]), dtype=torch.float32, device=self.dev)
         else:
             y = torch.empty(out_shape, dtype=torch.bfloat16, device=self.dev)
         st = (ctypes.c_longlong * 5)(*strides) if strides is not None else None
-        check(lib().ddit_conv_small(ptr(x), 1 if x_f32 else 0, st, ptr(w.contiguous()), ptr(b),
+        check(lib().ddit_conv_small(ptr(x), 1 if x_f32 else 0, st, ptr(w), ptr(b),
                                     ptr(y), B, T, H, Wd, Cin, Cout, kt, kh, kw, 1 if causal else 0,
                                     1 if out_cf else 0, crop[0], crop[1], stream_ptr()))
         self.launches += 1
@@ -131,7 +145,7 @@ class VAEDecoder:
         st = [zc.stride(0), zc.stride(1), zc.stride(2), zc.stride(3), zc.stride(4)]
         x = self._conv_small(zc, self.t_pq_w, self.t_pq_b, out_shape=(1, t1 - t0, h, w, C4),
                              x_f32=True, strides=st)
-        x = self._conv_small(x, self.W["t.conv1.weight"], self.W["t.conv1.bias"],
+        x = self._conv_small(x, self.small["t.conv1.weight"], self.W["t.conv1.bias"],
                              out_shape=(1, t1 - t0, h, w, self.W["t.conv1.weight"].shape[0]))
         for i in range(cfg.t_res_blocks):
             x = self._t_res(x, f"t.res_blocks.{i}")
@@ -197,7 +211,7 @@ class VAEDecoder:
                              causal=False)
         x = x.view(N, 1, h, w, 4)
         top = self.W["s.conv_in.weight"].shape[0]
-        x = self._conv_small(x, self.W["s.conv_in.weight"], self.W["s.conv_in.bias"],
+        x = self._conv_small(x, self.small["s.conv_in.weight"], self.W["s.conv_in.bias"],
                              out_shape=(N, 1, h, w, top), causal=False)
         x = self._s_res(x, "s.mid.resnets.0")
         x = self._mid_attention(x)
@@ -217,18 +231,39 @@ class VAEDecoder:
         B, T, H, Wd, C = y.shape
         # channels-first fp32 frames, 3 valid channels, cropped to (height, width)
         frames = torch.empty((1, 3, N, height, width), dtype=torch.float32, device=self.dev)
-        eye = torch.zeros((3, 1, 1, 1, 64), device=self.dev)
-        eye[0, 0, 0, 0, 0] = eye[1, 0, 0, 0, 1] = eye[2, 0, 0, 0, 2] = 1.0
-        st = [0, 1, H * Wd * C, Wd * C, C]
-        check(lib().ddit_conv_small(ptr(y), 0, (ctypes.c_longlong * 5)(*st), ptr(eye), None,
-                                    ptr(frames), 1, N, H, Wd, 64, 3, 1, 1, 1, 0, 1, height, width,
-                                    stream_ptr()))
+        check(lib().ddit_frames_out(ptr(y), ptr(frames), N, H, Wd, C, 3, height, width, stream_ptr()))
         self.launches += 1
         return frames
 
     # ---------------------------------------------------------------- pipeline
     def decode(self, z: torch.Tensor, num_frames: int, height: int, width: int,
                frames: tuple[int, int] | None = None) -> torch.Tensor:
+        """The decode below, replayed from a CUDA graph once a shape has been seen: the first call
+        per (latent shape, frames, size) runs eagerly and captures; later calls copy z into the
+        graph's input and replay its ~850 launches as one (LRU of ``graphs`` shapes; the graph
+        pool keeps that shape's activations resident). Same kernels, same bits as eager."""
+        if self.max_graphs <= 0:
+            return self.decode_eager(z, num_frames, height, width, frames)
+        key = (tuple(z.shape), tuple(z.stride()), num_frames, height, width, frames)
+        ent = self._graphs.pop(key, None)
+        if ent is None:
+            out = self.decode_eager(z, num_frames, height, width, frames)  # also the warm-up
+            static_z = z.clone()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                static_out = self.decode_eager(static_z, num_frames, height, width, frames)
+            self._graphs[key] = (g, static_z, static_out)
+            while len(self._graphs) > self.max_graphs:
+                self._graphs.pop(next(iter(self._graphs)))
+            return out
+        g, static_z, static_out = ent
+        self._graphs[key] = ent  # most recent last
+        static_z.copy_(z)
+        g.replay()
+        return static_out.clone()
+
+    def decode_eager(self, z: torch.Tensor, num_frames: int, height: int, width: int,
+                     frames: tuple[int, int] | None = None) -> torch.Tensor:
         """VideoAutoencoderPipeline.decode: z [1, 4, T, h, w] fp32 (device) ->
         video [1, 3, num_frames, height, width] fp32. ``frames=(a, b)``: only video frames
         [a, b) of the ``num_frames`` that z's micro-batches decode to (VAE DoP, ``vae_shard``)."""

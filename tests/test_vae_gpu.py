@@ -47,3 +47,26 @@ def test_full_width_vae_decode_matches_oracle(cuda):
     err = rel_l2(out.cpu(), ref)
     print(f"full-width vae 144p x16: relL2 {err:.2e}")
     assert err <= 3e-2
+
+
+def test_graph_replay_equals_eager(cuda):
+    """decode() captures a CUDA graph on the first call per shape and replays it afterwards: the
+    replay (new latent copied into the graph input) equals the eager decode bit for bit, and a
+    second shape evicts nothing it still needs."""
+    from paper_2506_13497_b200 import vae_weights as vw
+    from paper_2506_13497_b200.vae import VAEDecoder
+
+    cfg = vw.TINY_VAE
+    dec = VAEDecoder(cfg, vw.init_vae_weights(cfg), cuda, graphs=2)
+    g = torch.Generator().manual_seed(5)
+    zs = [torch.randn(1, 4, 4, 6, 10, generator=g).to(cuda) for _ in range(3)]
+    z2 = torch.randn(1, 4, 2, 5, 7, generator=g).to(cuda)
+    first = dec.decode(zs[0], 16, 48, 80)  # eager + capture
+    assert torch.equal(first, dec.decode_eager(zs[0], 16, 48, 80))
+    for z in zs[1:]:
+        rep = dec.decode(z, 16, 48, 80)
+        assert torch.equal(rep, dec.decode_eager(z, 16, 48, 80))
+    dec.decode(z2, 5, 40, 56)
+    assert torch.equal(dec.decode(z2, 5, 40, 56), dec.decode_eager(z2, 5, 40, 56))
+    assert torch.equal(dec.decode(zs[1], 16, 48, 80), dec.decode_eager(zs[1], 16, 48, 80))
+    assert len(dec._graphs) == 2
