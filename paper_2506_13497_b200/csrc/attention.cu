@@ -279,11 +279,8 @@ int attention_launch(const ddit_attn* a, cudaStream_t s) {
   p.scale_log2 = a->scale * 1.4426950408889634f;
   dim3 grid((a->Lq + BQ - 1) / BQ, a->heads, a->num_seqs);
   constexpr int smem = 5 * BQ * PITCH * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(flash_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static size_t attr[64] = {};
+  ensure_smem((const void*)flash_attn_kernel, smem, attr);
   flash_attn_kernel<<<grid, ATT_THREADS, smem, s>>>(p);
   return check_cuda("flash_attn_kernel");
 }

@@ -229,11 +229,8 @@ int temporal_attention_launch(const ddit_attn* a, cudaStream_t s) {
     return DDIT_E_INVALID;
   }
   auto kern = NT == 2 ? temporal_attn_kernel<2> : temporal_attn_kernel<4>;
-  static bool attr[2] = {false, false};
-  if (!attr[NT == 4]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr[NT == 4] = true;
-  }
+  static size_t attr[2][64] = {};
+  ensure_smem((const void*)kern, 227 * 1024, attr[NT == 4]);
   launch_pdl(kern, dim3(a->num_seqs), dim3(TA_THREADS), smem, s, p);
   return check_cuda("temporal_attn_kernel");
 }

@@ -11,6 +11,20 @@
 
 namespace ddit {
 
+// host: raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT device (function
+// attributes live in each device's context, so a process driving several GPUs sets it per
+// device); `done` is the call site's per-device record.
+inline cudaError_t ensure_smem(const void* kern, size_t bytes, size_t (&done)[64]) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (done[dev] >= bytes) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[dev] = bytes;
+  return e;
+}
+
 // ---------------------------------------------------------------- basic
 DDIT_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -329,11 +329,8 @@ template <int BN, bool RES>
 static int launch(const CUtensorMap& x, const CUtensorMap& w, const CUtensorMap& y,
                   const CUtensorMap& r, const Params& p, int grid, cudaStream_t s) {
   using C = Cfg<BN, RES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv_kernel<BN, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  static size_t attr[64] = {};
+  ensure_smem((const void*)conv_kernel<BN, RES>, C::SMEM, attr);
   conv_kernel<BN, RES><<<grid, THREADS, C::SMEM, s>>>(x, w, y, r, p);
   return check_cuda("conv_kernel");
 }

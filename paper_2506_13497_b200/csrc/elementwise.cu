@@ -404,11 +404,8 @@ int final_layer(const float* x, const float* fin, const float* Wf, const float* 
   if (Tl <= 0) return 0;
   if (4 * Cin > 16 || C % 4 || C > 32 * 4 * fl::MAXV) return -2;
   const size_t smem = ((size_t)4 * Cin * C + 4 * C) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(final_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  static size_t attr[64] = {};
+  ensure_smem((const void*)final_layer_kernel, smem, attr);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -688,11 +688,8 @@ static int fmha_poly() {
 
 template <int POLY>
 static int fmha_launch_t(const FmhaPlan* fp, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fmha_sm100_kernel<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, fm::SMEM);
-    attr = true;
-  }
+  static size_t attr[64] = {};
+  ensure_smem((const void*)fmha_sm100_kernel<POLY>, fm::SMEM, attr);
   launch_pdl(fmha_sm100_kernel<POLY>, fp->grid, dim3(fm::THREADS), fm::SMEM, s, fp->tmQa, fp->tmQb,
              fp->tmKVa, fp->tmKVb, fp->tmO, fp->p);
   return check_cuda("fmha_sm100_kernel");

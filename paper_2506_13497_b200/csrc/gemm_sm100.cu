@@ -1089,15 +1089,13 @@ void set_two_cta(int on) { g_two_cta = on ? 1 : 0; }
 template <int BN, int EPI>
 static int launch_t2(const GemmPlan* p, cudaStream_t s) {
   constexpr int smem = GemmCfg2<BN, EPI>::SMEM;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm2_bf16_tn_kernel<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static size_t attr[64] = {};
+  {
+    cudaError_t e = ensure_smem((const void*)gemm2_bf16_tn_kernel<BN, EPI>, smem, attr);
     if (e != cudaSuccess) {
       snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
       return -4;
     }
-    attr_set = true;
   }
   launch_pdl(gemm2_bf16_tn_kernel<BN, EPI>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
              p->tmO, p->tmR, p->tmO2, p->M, p->N, p->K, p->ep);
@@ -1113,15 +1111,13 @@ template <int BN, int EPI>
 static int launch_t(const GemmPlan* p, cudaStream_t s) {
   if (p->two_cta) return launch_t2<BN, EPI>(p, s);
   constexpr int smem = GemmCfg<BN, EPI>::SMEM;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static size_t attr[64] = {};
+  {
+    cudaError_t e = ensure_smem((const void*)gemm_bf16_tn_kernel<BN, EPI>, smem, attr);
     if (e != cudaSuccess) {
       snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
       return -4;
     }
-    attr_set = true;
   }
   launch_pdl(gemm_bf16_tn_kernel<BN, EPI>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
              p->tmO, p->tmR, p->tmO2, p->M, p->N, p->K, p->ep);

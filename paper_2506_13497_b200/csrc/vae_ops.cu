@@ -24,73 +24,128 @@ namespace ddit {
 //   gn_apply:    y = act(x*a + b), one FMA per element (+ SiLU as x*(0.5 + 0.5*tanh(x/2)), one MUFU
 //                op); the thread's channel vector is fixed, so its 16 coefficients stay in registers.
 constexpr int kGnUnroll = 4;       // vectors in flight per thread, apply
-constexpr int kGnPartUnroll = 8;   // and statistics
+constexpr int kGnPartUnroll = 8;   // statistics: partition granule (pixels per thread)
 
+// The block's pixels [p0, p1) of sample n are one contiguous byte range: it streams through a
+// ring of kGnStages 16 KB shared-memory stages filled by bulk async copies (one elected thread,
+// mbarrier completion), so ~48 KB per block are in flight without relying on per-thread loads.
+constexpr int kGnStageBytes = 16384, kGnStages = 3;
+constexpr int kGnPartSmem = kGnStages * kGnStageBytes + kGnStages * 8;
+
+DDIT_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Persistent: block b takes chunks (n, blk) = b, b + gridDim.x, ... of the N x nblk chunks, and its
+// ring runs across chunk boundaries (the next chunk's stages load while this one is reduced). A
+// chunk's sums do not depend on which block takes it (same per-thread order, same fixed fold).
 __global__ void __launch_bounds__(256)
-    gn_partial_kernel(const __nv_bfloat16* __restrict__ x, float2* __restrict__ partial, int P,
-                      int C, int G, int ppb, int nblk) {
-  const int n = blockIdx.y, blk = blockIdx.x;
+    gn_partial_kernel(const __nv_bfloat16* __restrict__ x, float2* __restrict__ partial, int N,
+                      int P, int C, int G, int ppb, int nblk) {
+  extern __shared__ __align__(128) uint8_t gn_smem[];
   const int cg = C / G;
   const int vecs = C / 8;
   const int step = 256 / vecs;
-  const int v = threadIdx.x % vecs;
-  const int p0 = blk * ppb;
-  const int p1 = min(p0 + ppb, P);
   __shared__ float2 red[256][8];
-  float sg[8], qg[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) sg[e] = qg[e] = 0.f;
-  const __nv_bfloat16* base = x + (size_t)n * P * C + v * 8;
-  for (int p = p0 + (int)threadIdx.x / vecs; p < p1; p += kGnPartUnroll * step) {
-    uint4 u[kGnPartUnroll];
-#pragma unroll
-    for (int k = 0; k < kGnPartUnroll; ++k)
-      u[k] = (p + k * step < p1) ? __ldcs(reinterpret_cast<const uint4*>(base + (size_t)(p + k * step) * C))
-                                 : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int k = 0; k < kGnPartUnroll; ++k) {
-      const uint32_t w[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = unpack_bf16(w[e]);
-        sg[2 * e] += f.x;
-        sg[2 * e + 1] += f.y;
-        qg[2 * e] = fmaf(f.x, f.x, qg[2 * e]);
-        qg[2 * e + 1] = fmaf(f.y, f.y, qg[2 * e + 1]);
-      }
-    }
-  }
-  // fold the 8 channels into their group(s): slot j holds group (v*8 + j*cg) / cg
-  const int gpv = cg >= 8 ? 1 : 8 / cg;  // groups per 8-channel vector
-  const int width = 8 / gpv;
-  for (int j = 0; j < gpv; ++j) {
-    float s = 0.f, q = 0.f;
-    for (int e = j * width; e < (j + 1) * width; ++e) {
-      s += sg[e];
-      q += qg[e];
-    }
-    red[threadIdx.x][j] = make_float2(s, q);
+  const uint4* ring = reinterpret_cast<const uint4*>(gn_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gn_smem + kGnStages * kGnStageBytes);
+  const int nchunks = N * nblk;
+  const uint32_t row_bytes = (uint32_t)C * 2;
+  auto chunk_bytes = [&](int c) -> uint32_t {
+    const int p0 = (c % nblk) * ppb;
+    return (uint32_t)(min(p0 + ppb, P) - p0) * row_bytes;
+  };
+  auto chunk_src = [&](int c) -> const char* {
+    return reinterpret_cast<const char*>(x + ((size_t)(c / nblk) * P + (size_t)(c % nblk) * ppb) * C);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGnStages; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
   }
   __syncthreads();
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    float s = 0.f, q = 0.f;
-    if (cg >= 8) {
-      const int vpg = cg / 8;
-      for (int k = 0; k < step; ++k)
-        for (int j = 0; j < vpg; ++j) {
-          const float2 r = red[k * vecs + g * vpg + j][0];
+  // producer cursor (thread 0 only): chunk ic, byte offset ioff, ring slot counter ig
+  int ic = blockIdx.x, ig = 0;
+  uint32_t ioff = 0;
+  auto issue_next = [&]() {
+    if (ic >= nchunks) return;
+    const uint32_t total = chunk_bytes(ic);
+    const uint32_t bytes = min((uint32_t)kGnStageBytes, total - ioff);
+    uint64_t* bar = &full[ig % kGnStages];
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(gn_smem + (ig % kGnStages) * kGnStageBytes, chunk_src(ic) + ioff, bytes, bar);
+    ++ig;
+    ioff += bytes;
+    if (ioff >= total) {
+      ioff = 0;
+      ic += gridDim.x;
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kGnStages; ++i) issue_next();
+  int g_cons = 0;  // consumer ring counter
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    float sg[8], qg[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sg[e] = qg[e] = 0.f;
+    const uint32_t total = chunk_bytes(c);
+    // stage offsets are multiples of 1024 vectors and 256 of C/8: thread t always sees channel
+    // vector t % (C/8)
+    for (uint32_t off = 0; off < total; off += kGnStageBytes, ++g_cons) {
+      mbar_wait(&full[g_cons % kGnStages], (g_cons / kGnStages) & 1);
+      const int nv = (int)(min((uint32_t)kGnStageBytes, total - off) / 16);
+      const uint4* sv = ring + (g_cons % kGnStages) * (kGnStageBytes / 16);
+      for (int i = threadIdx.x; i < nv; i += 256) {
+        const uint4 u = sv[i];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = unpack_bf16(w[e]);
+          sg[2 * e] += f.x;
+          sg[2 * e + 1] += f.y;
+          qg[2 * e] = fmaf(f.x, f.x, qg[2 * e]);
+          qg[2 * e + 1] = fmaf(f.y, f.y, qg[2 * e + 1]);
+        }
+      }
+      __syncthreads();  // stage consumed by every thread: refill its slot
+      if (threadIdx.x == 0) issue_next();
+    }
+    // fold the 8 channels into their group(s): slot j holds group (v*8 + j*cg) / cg
+    const int gpv = cg >= 8 ? 1 : 8 / cg;  // groups per 8-channel vector
+    const int width = 8 / gpv;
+    for (int j = 0; j < gpv; ++j) {
+      float s = 0.f, q = 0.f;
+      for (int e = j * width; e < (j + 1) * width; ++e) {
+        s += sg[e];
+        q += qg[e];
+      }
+      red[threadIdx.x][j] = make_float2(s, q);
+    }
+    __syncthreads();
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      float s = 0.f, q = 0.f;
+      if (cg >= 8) {
+        const int vpg = cg / 8;
+        for (int k = 0; k < step; ++k)
+          for (int j = 0; j < vpg; ++j) {
+            const float2 r = red[k * vecs + g * vpg + j][0];
+            s += r.x;
+            q += r.y;
+          }
+      } else {
+        for (int k = 0; k < step; ++k) {
+          const float2 r = red[k * vecs + g / gpv][g % gpv];
           s += r.x;
           q += r.y;
         }
-    } else {
-      for (int k = 0; k < step; ++k) {
-        const float2 r = red[k * vecs + g / gpv][g % gpv];
-        s += r.x;
-        q += r.y;
       }
+      partial[(size_t)c * G + g] = make_float2(s, q);
     }
-    partial[((size_t)n * nblk + blk) * G + g] = make_float2(s, q);
+    __syncthreads();  // red reused by the next chunk
   }
 }
 
@@ -421,8 +476,16 @@ DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* 
   nblk = (P + ppb - 1) / ppb;
   float2* partial = reinterpret_cast<float2*>(stats + (size_t)N * G * 2);
   float2* coef = partial + (size_t)N * nblk * G;
-  gn_partial_kernel<<<dim3(nblk, N), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), partial, P,
-                                                  C, G, ppb, nblk);
+  static size_t attr[64] = {};
+  ensure_smem((const void*)gn_partial_kernel, kGnPartSmem, attr);
+  static int sms[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int pgrid = std::max(1, std::min(N * nblk, 3 * sms[dev]));  // persistent, 3 per SM
+  gn_partial_kernel<<<pgrid, 256, kGnPartSmem, s>>>(static_cast<const __nv_bfloat16*>(x), partial, N,
+                                                    P, C, G, ppb, nblk);
   gn_finalize_kernel<<<N, 256, 0, s>>>(partial, coef, gamma, beta, P, C, G, nblk, eps);
   const size_t vpn = (size_t)P * (C / 8);
   const dim3 grid((unsigned)((vpn + 256 * kGnUnroll - 1) / (256 * kGnUnroll)), N);

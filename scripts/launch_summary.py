@@ -9,11 +9,12 @@ rows = list(csv.reader(open(sys.argv[1])))
 h = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 hd = rows[h]
 ki, vi, gi, ui = hd.index("Kernel Name"), hd.index("Metric Value"), hd.index("Grid Size"), hd.index("Metric Unit")
+mi = hd.index("Metric Name")
 scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
 agg = collections.defaultdict(lambda: [0, 0.0])
 grids = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[h + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
         continue
     ms = float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
     k = r[ki].split("(")[0][:60]
