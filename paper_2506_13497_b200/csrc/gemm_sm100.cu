@@ -30,6 +30,22 @@ static constexpr int kAccStride = 256;  // TMEM column offset of accumulator buf
 
 __host__ __device__ constexpr bool is_resid(int epi) { return epi == EPI_RESID || epi == EPI_RESID_COPY; }
 
+#ifndef DDIT_RSLOTS
+#define DDIT_RSLOTS 2
+#endif
+// DDIT_EPI_TRACE (experiment builds only): SM-clock timestamps of CTA 0's MMA issuer and first
+// epilogue warp per tile / sub-tile, read back with ddit_debug_trace()
+#ifdef DDIT_EPI_TRACE
+__device__ unsigned long long g_epi_trace[1024];
+#define EPI_TRACE(idx) \
+  do {                 \
+    if (blockIdx.x == 0) g_epi_trace[(idx) & 1023] = clock64(); \
+  } while (0)
+#else
+#define EPI_TRACE(idx) \
+  do {                 \
+  } while (0)
+#endif
 template <int BN, int EPI>
 struct EpiCfg {
   // staging bytes (two buffers) and sub-tile width (columns) per epilogue kind: bf16 outputs
@@ -39,7 +55,7 @@ struct EpiCfg {
   static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
   // gated residual: each epilogue warp runs its own ring of RSLOTS fp32 32x32 sub-tiles (loads run
   // RSLOTS-2 sub-tiles ahead) + three bf16 copy buffers (SW64): WARP_BYTES per warp
-  static constexpr int RSLOTS = is_resid(EPI) ? 2 : 0;
+  static constexpr int RSLOTS = is_resid(EPI) ? DDIT_RSLOTS : 0;
   // R >= 3: stores of sub-tile s-1 may still read while s runs (3 bf16 buffers, loads R-2 ahead);
   // R == 2: they must finish first (2 bf16 buffers, loads 1 ahead)
   static constexpr int RAHEAD = RSLOTS >= 3 ? RSLOTS - 2 : 1;
@@ -48,7 +64,11 @@ struct EpiCfg {
   // in one TMA store -- 64 B-row boxes store at a fraction of the bandwidth
   static constexpr int OB = EPI == EPI_RESID_COPY ? 4096 : 2048;
   static constexpr int WARP_BYTES = RSLOTS * 4096 + NOB * OB;
-  static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES : 2 * BUF;
+  // gated residual: the bias row and the B gate rows (all N columns) staged once per CTA, so the
+  // per-sub-tile column vectors are shared-memory broadcasts instead of cold L2 reads (consecutive
+  // tiles of a CTA have different column blocks)
+  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : 0;  // QKV: bias
+  static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES + COL_BYTES : 2 * BUF + COL_BYTES;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
 
@@ -65,7 +85,7 @@ struct GemmCfg {
   static_assert(B_BYTES % 1024 == 0, "B tile must keep 1024 B swizzle-atom alignment");
   static_assert(BN % 16 == 0 && BN <= 256, "invalid UMMA N");
   static_assert(BN % EpiCfg<BN, EPI>::SUB == 0, "BN must be a multiple of the epilogue sub-tile");
-  static_assert(STAGES >= 3, "pipeline too shallow");
+  static_assert(STAGES >= (DDIT_RSLOTS > 2 ? 2 : 3), "pipeline too shallow");
 };
 
 DDIT_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t* r) {
@@ -133,8 +153,35 @@ DDIT_DEV float gelu_fast(float x) {
 
 struct EpiCtx {
   int m_tiles, n_tiles, num_tiles;
-  int M;
+  int M, N;
 };
+
+// Stage bias[N] and gate[b][N] (b < ceil(M / rows_per_b)) into sCol (COL_BYTES) with the 128
+// epilogue threads; returns sCol, or nullptr when they do not fit (the epilogue then reads them
+// from global memory). Ends with the epilogue warps' named barrier.
+template <int COL_BYTES>
+DDIT_DEV const float* epi_stage_cols(const EpiParams& ep, float* sCol, int M, int N, int tid) {
+  const int nb = ep.gate ? (M + ep.rows_per_b - 1) / ep.rows_per_b : 0;
+  const bool fits = (size_t)(1 + nb) * N * 4 <= (size_t)COL_BYTES;
+  if (fits) {  // all loads first (independent, one latency), then the shared stores
+    constexpr int PER = COL_BYTES / 4 / 128;
+    const int total = (1 + nb) * N;
+    float v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = tid + 128 * k;
+      const int row = idx / N, col = idx - row * N;
+      v[k] = idx >= total ? 0.f
+             : row == 0   ? (ep.bias ? __ldg(ep.bias + col) : 0.f)
+                          : __ldg(ep.gate + (size_t)(row - 1) * ep.gate_stride + col);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (tid + 128 * k < total) sCol[tid + 128 * k] = v[k];
+  }
+  epi_bar();
+  return fits ? sCol : nullptr;
+}
 
 // The sequence of 128x32 residual sub-tiles this CTA's epilogue consumes: sub-tile j belongs to
 // the CTA's (j / NS)-th tile (tile0 + i * tstride) at column block j % NS.
@@ -178,6 +225,13 @@ DDIT_DEV void mbar_arrive_cl(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
                : "memory");
 }
+// accumulator hand-back (TMEM empty): no memory to publish -- the tcgen05.wait::ld before and
+// tcgen05.fence::before_thread_sync order the TMEM reads -- so a relaxed arrive; a release arrive
+// would wait for the thread's (and, through the fence, the warp's) outstanding bulk stores
+DDIT_DEV void mbar_arrive_cl_relaxed(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
+               : "memory");
+}
 DDIT_DEV uint32_t cluster_addr(const void* p, uint32_t rank) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
@@ -212,7 +266,7 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
     if (sub == NS - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty_cl);
+      if (lane == 31) mbar_arrive_cl_relaxed(tempty_cl);
     }
     const int col0 = n0 + sub * SUB;
     float v[SUB];
@@ -300,7 +354,7 @@ template <int BN, int EPI>
 DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const CUtensorMap* tmO2,
                              uint8_t* sE, uint64_t* rbar, uint32_t taddr, int ew, int lane,
                              int m0, int n0, const EpiCtx& cx, const ResidStream& rs,
-                             int& cnt, uint32_t tempty_cl) {
+                             int& cnt, uint32_t tempty_cl, const float* sCol) {
   constexpr int NS = BN / 32;
   constexpr bool COPY = EPI == EPI_RESID_COPY;
   static_assert(!COPY || NS % 2 == 0, "paired bf16 copy needs BN % 64 == 0");
@@ -312,6 +366,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
   const int row = m0 + ew * 32 + lane;
   const int grow = row < cx.M ? row : cx.M - 1;
   const float* gate_row = ep.gate ? ep.gate + (size_t)(grow / ep.rows_per_b) * ep.gate_stride : nullptr;
+  const float* s_gate = sCol && ep.gate ? sCol + (size_t)(1 + grow / ep.rows_per_b) * cx.N : nullptr;
   // fused exchange: lane l copies rows 4i + l/8 (i < 8), 16 B chunk l%8 of each sub-tile row
   float* xrow[8];
   if (ep.xch) {
@@ -331,43 +386,60 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
     const int col0 = n0 + sub * 32;
     // column vectors first: their L2 latency overlaps the waits below
     float4 bv[8], gv[8];
+    if (sCol) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      bv[j] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      gv[j] = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
-                       : make_float4(1.f, 1.f, 1.f, 1.f);
+      for (int j = 0; j < 8; ++j) {
+        bv[j] = reinterpret_cast<const float4*>(sCol + col0)[j];
+        gv[j] = s_gate ? reinterpret_cast<const float4*>(s_gate + col0)[j] : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bv[j] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[j] = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
+                         : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
     }
     if (lane == 0) {
       // this warp's stores up to sub-tile cnt-1-(NOB-2) have read their smem, so the ring slot
       // of sub-tile cnt+RAHEAD and the next bf16 buffer are free again
       constexpr int AH = Cfg::RAHEAD;
       bulk_wait_read<Cfg::NOB - 2>();
+      if (ew == 0) EPI_TRACE(384 + 16 * (cnt / NS) + sub);
       resid_issue<R>(rs, NS, cnt + AH, ew * 32, tmR, wbase, wbar);
     }
+    if (ew == 0 && lane == 0) EPI_TRACE(256 + 16 * (cnt / NS) + 2 * sub);
     mbar_wait(&wbar[slot], (cnt / R) & 1);
+    if (ew == 0 && lane == 0) EPI_TRACE(256 + 16 * (cnt / NS) + 2 * sub + 1);
     uint32_t r[32];
     tmem_ld_x32(taddr + sub * 32, r);
     tmem_ld_wait();
+    if (ew == 0 && lane == 0) EPI_TRACE(512 + 16 * (cnt / NS) + sub);
     if (sub == NS - 1) {
+      // lane 31 arrives: its release has no outstanding TMA issue / global traffic to order
+      // (lane 0 issues the warp's bulk copies), so it does not stall the warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty_cl);
+      if (lane == 31) mbar_arrive_cl_relaxed(tempty_cl);
     }
     const uint32_t rbase = smem_u32(rb);
     float nv[32];
+    float4 xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xv[j] = ld_shared_f4(rbase + sw128(rit, j));  // all loads in flight
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float4 b = bv[j], g = gv[j];
-      const uint32_t a = rbase + sw128(rit, j);
-      const float4 x = ld_shared_f4(a);
+      const float4 b = bv[j], g = gv[j], x = xv[j];
       nv[4 * j + 0] = x.x + g.x * (__uint_as_float(r[4 * j + 0]) + b.x);
       nv[4 * j + 1] = x.y + g.y * (__uint_as_float(r[4 * j + 1]) + b.y);
       nv[4 * j + 2] = x.z + g.z * (__uint_as_float(r[4 * j + 2]) + b.z);
       nv[4 * j + 3] = x.w + g.w * (__uint_as_float(r[4 * j + 3]) + b.w);
-      st_shared_v4(a, __float_as_uint(nv[4 * j]), __float_as_uint(nv[4 * j + 1]),
-                   __float_as_uint(nv[4 * j + 2]), __float_as_uint(nv[4 * j + 3]));
     }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      st_shared_v4(rbase + sw128(rit, j), __float_as_uint(nv[4 * j]), __float_as_uint(nv[4 * j + 1]),
+                   __float_as_uint(nv[4 * j + 2]), __float_as_uint(nv[4 * j + 3]));
     if (COPY) {  // chunks 4h..4h+3 of the pair's 128 B row, h = sub-tile parity
       const uint32_t obase = smem_u32(ob);
       const int h = cnt & 1;
@@ -384,6 +456,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
                      pack_bf16(nv[8 * j + 2], nv[8 * j + 3]), pack_bf16(nv[8 * j + 4], nv[8 * j + 5]),
                      pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
     }
+    if (ew == 0 && lane == 0) EPI_TRACE(768 + 16 * (cnt / NS) + sub);
     if (ep.xch) {  // rows go to their owner rank (peer stores), 4 whole 128 B rows per instruction
       __syncwarp();
 #pragma unroll
@@ -408,6 +481,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
         bulk_commit();
       }
     }
+    if (ew == 0 && lane == 0) EPI_TRACE(640 + 16 * (cnt / NS) + sub);
     ++cnt;
   }
 }
@@ -417,7 +491,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
 // q,k: bias -> per-head RMSNorm (weight) -> optional interleaved RoPE by frame index.
 DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
                            uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
-                           uint32_t tempty_cl, int lane) {
+                           uint32_t tempty_cl, int lane, const float* sCol) {
   constexpr int HD = 72;
   const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
   const int row = m0 + rit;
@@ -439,14 +513,15 @@ DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t*
     if (h == 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty_cl);
+      if (lane == 31) mbar_arrive_cl_relaxed(tempty_cl);
     }
     const int c0 = n0 + h * HD;
     float v[72];
     float ss = 0.f;
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + c0) + q);
+      const float4 b = sCol ? reinterpret_cast<const float4*>(sCol + c0)[q]
+                            : __ldg(reinterpret_cast<const float4*>(ep.bias + c0) + q);
       v[4 * q + 0] = __uint_as_float(r[4 * q + 0]) + b.x;
       v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + b.y;
       v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + b.z;
@@ -521,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = lane_id();
   EpiCtx cx;
   cx.M = M;
+  cx.N = N;
   cx.m_tiles = (M + BM - 1) / BM;
   cx.n_tiles = N / BN;
   cx.num_tiles = cx.m_tiles * cx.n_tiles;
@@ -614,8 +690,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int cnt = 0;
     const ResidStream rs{(int)blockIdx.x, (int)gridDim.x, num_tiles, n_tiles, BM, 0};
+    const float* sCol = nullptr;
+    if constexpr (EPI == EPI_QKV)
+      sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
+          ep, reinterpret_cast<float*>(sE + 2 * EpiCfg<BN, EPI>::BUF), M, N, ew * 32 + lane);
     if constexpr (is_resid(EPI)) {
       constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
+      sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
+          ep, reinterpret_cast<float*>(sE + 4 * EpiCfg<BN, EPI>::WARP_BYTES), M, N, ew * 32 + lane);
       if (elected) {  // residual tiles 0 and 1 into L2
         resid_prefetch_l2<BN>(rs, 0, &tmO);
         resid_prefetch_l2<BN>(rs, 1, &tmO);
@@ -632,14 +714,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
         ++tix;
       }
+      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1));
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1) + 1);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
-        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
       } else if constexpr (is_resid(EPI)) {
-        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
+        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
@@ -733,6 +817,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   EpiCtx cx;
   cx.M = M;
+  cx.N = N;
   cx.m_tiles = (M + BM2 - 1) / BM2;
   cx.n_tiles = N / BN;
   cx.num_tiles = cx.m_tiles * cx.n_tiles;
@@ -799,13 +884,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += nclusters) {
+      int tt = 0;
+      for (int tile = cid; tile < num_tiles; tile += nclusters, ++tt) {
+        if (lane == 0) EPI_TRACE(2 * tt);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (lane == 0) EPI_TRACE(2 * tt + 1);
         const uint32_t d_tmem = tmem_base + acc * kAccStride;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (lane == 0 && kb == 0) EPI_TRACE(64 + 2 * tt);
+          if (lane == 0 && kb == k_blocks - 1) EPI_TRACE(64 + 2 * tt + 1);
           if (elect_one()) {
             const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
             const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
@@ -834,8 +924,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     int cnt = 0;
     const ResidStream rs{cid, nclusters, num_tiles, n_tiles, BM2, (int)rank * BM};
+    const float* sCol = nullptr;
+    if constexpr (EPI == EPI_QKV)
+      sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
+          ep, reinterpret_cast<float*>(sE + 2 * EpiCfg<BN, EPI>::BUF), M, N, ew * 32 + lane);
     if constexpr (is_resid(EPI)) {
       constexpr int R = EpiCfg<BN, EPI>::RSLOTS;
+      sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
+          ep, reinterpret_cast<float*>(sE + 4 * EpiCfg<BN, EPI>::WARP_BYTES), M, N, ew * 32 + lane);
       if (elected) {  // residual tiles 0 and 1 into L2
         resid_prefetch_l2<BN>(rs, 0, &tmO);
         resid_prefetch_l2<BN>(rs, 1, &tmO);
@@ -852,14 +948,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
         ++tix;
       }
+      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1));
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1) + 1);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
-        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
       } else if constexpr (is_resid(EPI)) {
-        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl);
+        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
         epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
       }
@@ -1177,3 +1275,8 @@ int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
 }
 
 }  // namespace ddit
+#ifdef DDIT_EPI_TRACE
+extern "C" __attribute__((visibility("default"))) int ddit_debug_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, ddit::g_epi_trace, sizeof(unsigned long long) * (n < 1024 ? n : 1024));
+}
+#endif
