@@ -67,7 +67,9 @@ struct EpiCfg {
   // gated residual: the bias row and the B gate rows (all N columns) staged once per CTA, so the
   // per-sub-tile column vectors are shared-memory broadcasts instead of cold L2 reads (consecutive
   // tiles of a CTA have different column blocks)
-  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : 0;  // QKV: bias
+  // QKV: bias; plain epilogues: bias up to 2048 columns, not at BN 256 (its mainloop stage count
+  // would drop, and those GEMMs are MMA-bound)
+  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : BN < 256 ? 8192 : 0;
   static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES + COL_BYTES : 2 * BUF + COL_BYTES;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
@@ -250,7 +252,7 @@ DDIT_DEV void cluster_sync_all() {
 template <int BN, int EPI>
 DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
                              uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
-                             uint32_t tempty_cl, int lane) {
+                             uint32_t tempty_cl, int lane, const float* sCol) {
   constexpr int SUB = EpiCfg<BN, EPI>::SUB;
   constexpr int NS = BN / SUB;
 #pragma unroll 1
@@ -272,8 +274,9 @@ DDIT_DEV void epi_plain_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_
     float v[SUB];
 #pragma unroll
     for (int q = 0; q < SUB / 4; ++q) {
-      float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + q)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 b = sCol     ? reinterpret_cast<const float4*>(sCol + col0)[q]
+                 : ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + q)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
       v[4 * q + 0] = __uint_as_float(r[4 * q + 0]) + b.x;
       v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + b.y;
       v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + b.z;
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int cnt = 0;
     const ResidStream rs{(int)blockIdx.x, (int)gridDim.x, num_tiles, n_tiles, BM, 0};
     const float* sCol = nullptr;
-    if constexpr (EPI == EPI_QKV)
+    if constexpr (!is_resid(EPI) && EpiCfg<BN, EPI>::COL_BYTES > 0)
       sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
           ep, reinterpret_cast<float*>(sE + 2 * EpiCfg<BN, EPI>::BUF), M, N, ew * 32 + lane);
     if constexpr (is_resid(EPI)) {
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if constexpr (is_resid(EPI)) {
         epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
-        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -925,7 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int cnt = 0;
     const ResidStream rs{cid, nclusters, num_tiles, n_tiles, BM2, (int)rank * BM};
     const float* sCol = nullptr;
-    if constexpr (EPI == EPI_QKV)
+    if constexpr (!is_resid(EPI) && EpiCfg<BN, EPI>::COL_BYTES > 0)
       sCol = epi_stage_cols<EpiCfg<BN, EPI>::COL_BYTES>(
           ep, reinterpret_cast<float*>(sE + 2 * EpiCfg<BN, EPI>::BUF), M, N, ew * 32 + lane);
     if constexpr (is_resid(EPI)) {
@@ -959,7 +962,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       } else if constexpr (is_resid(EPI)) {
         epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
-        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane);
+        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -1,6 +1,6 @@
 """Link an experimental variant of libddit.so: one source recompiled with extra nvcc flags, the
 other objects reused from the regular build (run build() first).
-Usage: python scripts/build_variant.py NAME SOURCE.cu -DFOO=1 ...  ->  paper_2506_13497_b200/libddit_NAME.so
+Usage: python scripts/build_variant.py NAME SOURCE.cu|/abs/path/SOURCE.cu -DFOO=1 ...  ->  paper_2506_13497_b200/libddit_NAME.so
 (load it with DDIT_LIB=paper_2506_13497_b200/libddit_NAME.so)."""
 import subprocess
 import sys
@@ -14,7 +14,8 @@ b.build(verbose=False)
 out_dir = b.BUILD.parent / f"var_{name}"
 out_dir.mkdir(parents=True, exist_ok=True)
 obj = out_dir / (Path(src).stem + ".o")
-subprocess.run([b.NVCC, *b.ARCH, *b.FLAGS, *extra, "-c", str(b.CSRC / src), "-o", str(obj)], check=True)
+src_path = Path(src) if Path(src).is_absolute() else b.CSRC / src  # absolute: e.g. an older revision
+subprocess.run([b.NVCC, *b.ARCH, *b.FLAGS, *extra, "-c", str(src_path), "-o", str(obj)], check=True)
 objs = [obj if o.stem == obj.stem else o for o in (b.BUILD / (s.stem + ".o") for s in b._sources())]
 lib = b.PKG / f"libddit_{name}.so"
 subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", str(lib), *map(str, objs), "-cudart", "shared",
