@@ -57,6 +57,12 @@ DDIT_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 DDIT_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// arrive without release semantics: for hand-backs that publish no memory (e.g. a TMEM
+// accumulator after tcgen05.wait::ld + tcgen05.fence::before_thread_sync); a release arrive waits
+// for the thread's outstanding memory operations (bulk stores included)
+DDIT_DEV void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 DDIT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(

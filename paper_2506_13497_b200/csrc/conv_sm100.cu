@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (sub == NS - 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 31) mbar_arrive_relaxed(&tempty[acc]);
         }
         const int col0 = tc.n0 + sub * 64;
 #pragma unroll
