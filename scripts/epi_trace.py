@@ -15,7 +15,8 @@ from paper_2506_13497_b200 import _lib, kernels
 dev = torch.device("cuda:0")
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 1152
 copy = len(sys.argv) > 2 and sys.argv[2] == "1"
-M, N = 2 * 6075, 1152
+qkv = len(sys.argv) > 2 and sys.argv[2] == "qkv"  # QKV shape + epilogue: MMA-side events only
+M, N = 2 * 6075, (3456 if qkv else 1152)
 a = torch.randn(M, K, device=dev).bfloat16()
 w = (torch.randn(N, K, device=dev) / math.sqrt(K)).bfloat16()
 bias = torch.zeros(N, device=dev)
@@ -28,7 +29,13 @@ L.ddit_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 for it in range(3):
     flush.zero_()
     torch.cuda.synchronize()
-    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, out2=o2)
+    if qkv:
+        qw = torch.ones(72, device=dev)
+        tab = torch.randn(15, 36, 2, device=dev)
+        kernels.gemm(a, w, epi=_lib.EPI_QKV, bias=bias, qnorm_w=qw, knorm_w=qw, hidden=1152, rope_tab=tab,
+                     rope_T=15, rope_S=405, bn=144)
+    else:
+        kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, out2=o2)
     torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 1024)()
 L.ddit_debug_trace(buf, 1024)
@@ -38,6 +45,11 @@ base = min(v for v in t if v)
 us = lambda v: (v - base) / clk if v else float("nan")
 print("events:", us(t[0]), us(t[1]), us(t[64]), us(t[65]), us(t[128]), us(t[129]))
 ntiles = sum(1 for i in range(32) if t[2 * i])
+if qkv:
+    for i in range(ntiles):
+        print(f"tile {i}: mma wait-empty {us(t[2*i]):7.2f} -> {us(t[2*i+1]):7.2f} (waited {us(t[2*i+1]) - us(t[2*i]):5.2f})"
+              f"  kb0 {us(t[64+2*i]):7.2f} kblast {us(t[64+2*i+1]):7.2f}")
+    sys.exit(0)
 for i in range(ntiles):
     print(f"tile {i}: mma wait-empty {us(t[2*i]):7.2f} -> {us(t[2*i+1]):7.2f}  kb0 {us(t[64+2*i]):7.2f} kblast {us(t[64+2*i+1]):7.2f} | "
           f"epi wait-full {us(t[128+2*i]):7.2f} -> {us(t[128+2*i+1]):7.2f}")
