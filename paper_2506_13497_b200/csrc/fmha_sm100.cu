@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[g]);
+        if (lane == 31) mbar_arrive_relaxed(&s_free[g]);  // lane 0 of warp 4/8 issues the O bulk stores
         const int valid = min(BKV, p.Lk - j * BKV);
         const bool full = valid == BKV;
         float mx8[8];
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         }
         if (has1) {  // hand the MUFU turn to the other group
           __syncwarp();
-          if (lane == 0) mbar_arrive(&exp_tok[g ^ 1]);
+          if (lane == 31) mbar_arrive_relaxed(&exp_tok[g ^ 1]);
           ++tk;
         }
         if (j > 0) {
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[g]);
+        if (lane == 31) mbar_arrive(&p_full[g]);  // release (P stores), from a lane without bulk copies
       }
       // ---- unit epilogue: O / l -> bf16 -> staging (the P buffer, 144 B rows) -> TMA store
       mbar_wait(&pv_done[g], (n - 1) & 1);
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       const float l = __uint_as_float(o[72]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[g]);
+      if (lane == 31) mbar_arrive_relaxed(&o_free[g]);
       const float inv = l > 0.f ? 1.f / l : 0.f;
       const uint32_t obase = smem_u32(pbuf) + row * 144;
 #pragma unroll
