@@ -67,9 +67,9 @@ struct EpiCfg {
   // gated residual: the bias row and the B gate rows (all N columns) staged once per CTA, so the
   // per-sub-tile column vectors are shared-memory broadcasts instead of cold L2 reads (consecutive
   // tiles of a CTA have different column blocks)
-  // QKV: bias; plain epilogues: bias up to 2048 columns, not at BN 256 (its mainloop stage count
-  // would drop, and those GEMMs are MMA-bound)
-  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : BN < 256 ? 8192 : 0;
+  // QKV: bias. Plain epilogues keep __ldg: staging their bias cost 1.3 ms per 144p step (small-M
+  // GEMMs have one or two tiles per CTA, so the per-CTA staging is not amortised)
+  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : 0;
   static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES + COL_BYTES : 2 * BUF + COL_BYTES;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
