@@ -63,7 +63,10 @@ struct EpiCfg {
   // EPI_RESID_COPY: the bf16 copy of a PAIR of sub-tiles (32 rows x 64 cols, 128 B rows) leaves
   // in one TMA store -- 64 B-row boxes store at a fraction of the bandwidth
   static constexpr int OB = EPI == EPI_RESID_COPY ? 4096 : 2048;
-  static constexpr int WARP_BYTES = RSLOTS * 4096 + NOB * OB;
+  // EPI_RESID with BN % 64 == 0 never has a bf16 copy (the plan turns out2 into EPI_RESID_COPY),
+  // so its copy buffers are not allocated: the smem goes back to the mainloop (fc2: 6 stages)
+  static constexpr bool HAS_OB = EPI == EPI_RESID_COPY || (EPI == EPI_RESID && BN % 64 != 0);
+  static constexpr int WARP_BYTES = RSLOTS * 4096 + (HAS_OB ? NOB * OB : 0);
   // gated residual: the bias row and the B gate rows (all N columns) staged once per CTA, so the
   // per-sub-tile column vectors are shared-memory broadcasts instead of cold L2 reads (consecutive
   // tiles of a CTA have different column blocks)
@@ -385,7 +388,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
     uint8_t* rb = wbase + slot * 4096;
     // bf16 copy buffer: per sub-tile (RESID) or per sub-tile pair (COPY; pairs never straddle a
     // tile because NS is even and cnt counts sub-tiles from 0)
-    uint8_t* ob = wbase + R * 4096 + ((COPY ? cnt >> 1 : cnt) % Cfg::NOB) * Cfg::OB;
+    uint8_t* ob = Cfg::HAS_OB ? wbase + R * 4096 + ((COPY ? cnt >> 1 : cnt) % Cfg::NOB) * Cfg::OB : nullptr;
     const int col0 = n0 + sub * 32;
     // column vectors first: their L2 latency overlaps the waits below
     float4 bv[8], gv[8];
@@ -451,7 +454,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
         st_shared_v4(obase + sw128(rit, 4 * h + j), pack_bf16(nv[8 * j], nv[8 * j + 1]),
                      pack_bf16(nv[8 * j + 2], nv[8 * j + 3]), pack_bf16(nv[8 * j + 4], nv[8 * j + 5]),
                      pack_bf16(nv[8 * j + 6], nv[8 * j + 7]));
-    } else if (ep.out2) {
+    } else if (Cfg::HAS_OB && ep.out2) {
       const uint32_t obase = smem_u32(ob);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -478,7 +481,7 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
         tma_store_2d(tmR, rb, col0, m0 + ew * 32);
         if (COPY) {
           if (cnt & 1) tma_store_2d(tmO2, ob, col0 - 32, m0 + ew * 32);
-        } else if (ep.out2) {
+        } else if (Cfg::HAS_OB && ep.out2) {
           tma_store_2d(tmO2, ob, col0, m0 + ew * 32);
         }
         bulk_commit();
