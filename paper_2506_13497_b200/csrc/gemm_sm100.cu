@@ -72,7 +72,8 @@ struct EpiCfg {
   // tiles of a CTA have different column blocks)
   // QKV: bias. Plain epilogues keep __ldg: staging their bias cost 1.3 ms per 144p step (small-M
   // GEMMs have one or two tiles per CTA, so the per-CTA staging is not amortised)
-  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 16384 : 0;
+  // sized to the XL/2 need (3 x 1152 or 3456 floats = 13.5 KB), so QKV keeps 7 mainloop stages
+  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 13824 : 0;
   static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES + COL_BYTES : 2 * BUF + COL_BYTES;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
