@@ -111,3 +111,20 @@ def test_gemm_qkv_epilogue(cuda, rope):
         q, k = rot(q), rot(k)
     ref = torch.stack([q, k, v], 1).view(M, 3 * C)
     assert rel_l2(out, ref) < 5e-3
+
+
+@pytest.mark.parametrize("nb,N", [(4, 576), (4, 1152), (3, 1152)])
+def test_gemm_resid_gate_many_batches(cuda, nb, N):
+    """Gate rows for more than two samples: staged in shared memory when (1 + nb) * N floats fit
+    (nb = 4, N = 576), read from global memory otherwise (N = 1152); ragged last sample (nb = 3)."""
+    from paper_2506_13497_b200 import kernels, _lib
+
+    M, K = 1300, 1152
+    rows_per_b = -(-M // nb)
+    a, w, bias = _inputs(M, N, K, cuda, seed=9)
+    x = torch.randn(M, N, device=cuda)
+    gate = torch.randn(nb, N, device=cuda)
+    x0 = x.clone()
+    kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=rows_per_b, bn=192)
+    b = torch.arange(M, device=cuda) // rows_per_b
+    assert rel_l2(x, x0 + gate[b] * (a.float() @ w.float().T + bias)) < 1e-5
