@@ -16,7 +16,8 @@ dev = torch.device("cuda:0")
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 1152
 copy = len(sys.argv) > 2 and sys.argv[2] == "1"
 qkv = len(sys.argv) > 2 and sys.argv[2] == "qkv"  # QKV shape + epilogue: MMA-side events only
-M, N = 2 * 6075, (3456 if qkv else 1152)
+fc1 = len(sys.argv) > 2 and sys.argv[2] == "fc1"  # fc1 shape + GELU epilogue: MMA-side events only
+M, N = 2 * 6075, (3456 if qkv else 4608 if fc1 else 1152)
 a = torch.randn(M, K, device=dev).bfloat16()
 w = (torch.randn(N, K, device=dev) / math.sqrt(K)).bfloat16()
 bias = torch.zeros(N, device=dev)
@@ -29,7 +30,9 @@ L.ddit_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 for it in range(3):
     flush.zero_()
     torch.cuda.synchronize()
-    if qkv:
+    if fc1:
+        kernels.gemm(a, w, epi=_lib.EPI_GELU_BF16, bias=bias)
+    elif qkv:
         qw = torch.ones(72, device=dev)
         tab = torch.randn(15, 36, 2, device=dev)
         kernels.gemm(a, w, epi=_lib.EPI_QKV, bias=bias, qnorm_w=qw, knorm_w=qw, hidden=1152, rope_tab=tab,
@@ -45,7 +48,7 @@ base = min(v for v in t if v)
 us = lambda v: (v - base) / clk if v else float("nan")
 print("events:", us(t[0]), us(t[1]), us(t[64]), us(t[65]), us(t[128]), us(t[129]))
 ntiles = sum(1 for i in range(32) if t[2 * i])
-if qkv:
+if qkv or fc1:
     for i in range(ntiles):
         print(f"tile {i}: mma wait-empty {us(t[2*i]):7.2f} -> {us(t[2*i+1]):7.2f} (waited {us(t[2*i+1]) - us(t[2*i]):5.2f})"
               f"  kb0 {us(t[64+2*i]):7.2f} kblast {us(t[64+2*i+1]):7.2f}")
