@@ -220,6 +220,10 @@ DDIT_API int ddit_step_phase(ddit_req* r, int phase, void* stream);
 DDIT_API int ddit_step_end(ddit_req* r, float* z_local, int step, void* stream);
 /* Cross-rank barrier after a push (no-op at DoP 1). */
 DDIT_API int ddit_step_barrier(ddit_req* r, void* stream);
+/* Health of a DoP > 1 request after its stream ran (synchronises `stream`): the barrier spin is
+ * bounded (env DDIT_XCH_TIMEOUT_MS, default 20000); status = 0 ok, or 1 + the rank whose flag
+ * never arrived, returned with DDIT_E_CONFIG. */
+DDIT_API int ddit_request_status(ddit_req* r, void* stream, uint32_t* status);
 
 /* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);

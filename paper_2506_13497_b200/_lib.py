@@ -146,6 +146,7 @@ _SIGNATURES = {
     "ddit_step_phase": [vp, ci, vp],
     "ddit_step_end": [vp, vp, ci, vp],
     "ddit_step_barrier": [vp, vp],
+    "ddit_request_status": [vp, vp, ctypes.POINTER(ctypes.c_uint32)],
     "ddit_request_timestep": [vp, ci, ctypes.POINTER(cf), ctypes.POINTER(cf)],
     "ddit_request_profile": [vp, ci],
     "ddit_request_set_option": [vp, ci, ci],

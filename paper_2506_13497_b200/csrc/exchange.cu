@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "exchange.cuh"
 
+#include <cstdlib>
+
 namespace ddit {
 
 DDIT_DEV void signal_peers(const ExchangeSync& sync) {
@@ -107,20 +109,45 @@ int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S
   return 1;
 }
 
-// Wait until every rank q published this rank's current epoch into slot q.
-__global__ void flag_wait_kernel(const uint32_t* flags, const uint32_t* epoch_p, int P) {
+// Wait until every rank q published this rank's current epoch into slot q. The spin is bounded
+// (globaltimer): a peer that never signals (dead process, wedged GPU) sets *status to
+// DDIT_XCH_TIMEOUT and the kernel returns, so the stream drains and the host reads the error
+// (ddit_request_status) instead of the GPU hanging.
+__global__ void flag_wait_kernel(const uint32_t* flags, const uint32_t* epoch_p, int P,
+                                 uint32_t* status, unsigned long long timeout_ns) {
   const int q = threadIdx.x;
   if (q >= P) return;
   const uint32_t epoch = *epoch_p;
   const uint32_t* mine = flags + q;
   uint32_t v;
-  do {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int spin = 0;; ++spin) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
-  } while ((int32_t)(v - epoch) < 0);
+    if ((int32_t)(v - epoch) >= 0) return;
+    if ((spin & 1023) == 1023) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        if (status) atomicMax(status, 1u + (uint32_t)q);  // 1 + the rank that never signalled
+        return;
+      }
+    }
+  }
 }
 
-int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, cudaStream_t s) {
-  flag_wait_kernel<<<1, 32, 0, s>>>(own_flags, epoch, P);
+static unsigned long long flag_timeout_ns() {
+  static unsigned long long ns = 0;
+  if (ns == 0) {
+    const char* e = getenv("DDIT_XCH_TIMEOUT_MS");
+    const double ms = e ? atof(e) : 20000.0;
+    ns = (unsigned long long)((ms > 0 ? ms : 20000.0) * 1e6);
+  }
+  return ns;
+}
+
+int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, uint32_t* status,
+              cudaStream_t s) {
+  flag_wait_kernel<<<1, 32, 0, s>>>(own_flags, epoch, P, status, flag_timeout_ns());
   return 1;
 }
 

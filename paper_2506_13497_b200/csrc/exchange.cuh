@@ -26,5 +26,7 @@ int exchange_sp_to_tp(const float* src, const PeerPtrs& dst, int B, int T, int S
                       int t_lo, int Tl, const ExchangeSync& sync, cudaStream_t s);
 int exchange_tp_to_sp(const float* src, const PeerPtrs& dst, int B, int T, int S, int C, int P,
                       int s_lo, int Sl, const ExchangeSync& sync, cudaStream_t s);
-int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, cudaStream_t s);
+// Bounded wait (DDIT_XCH_TIMEOUT_MS, default 20 s): on timeout *status = 1 + the silent rank.
+int flag_wait(const uint32_t* own_flags, const uint32_t* epoch, int P, uint32_t* status,
+              cudaStream_t s);
 }  // namespace ddit

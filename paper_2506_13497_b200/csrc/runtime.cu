@@ -616,8 +616,7 @@ static int embed_text(ddit_req* r, const float* y_cond, cudaStream_t s) {
                              2 * c.hidden, c.hidden, EPI_BF16, e, pick_bn(2 * c.hidden))) ||
         (rc = launch(gp, s))) {
       set_error("cross kv: %s", gemm_last_error());
-      delete r;
-      return DDIT_E_CUDA;
+      return DDIT_E_CUDA;  // r stays owned by the caller (ddit_request_open frees it on failure)
     }
   }
   return check_cuda("embed_text");
@@ -707,7 +706,13 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
 
 DDIT_API void ddit_request_close(ddit_req* r) { delete r; }
 
+// On failure the request stays open and owned by the caller (its text state is undefined until
+// a later set_text / copy_text succeeds); it is never freed here.
 DDIT_API int ddit_request_set_text(ddit_req* r, const float* y_cond, void* stream) {
+  if (!r || !y_cond) {
+    set_error("ddit_request_set_text: null argument");
+    return DDIT_E_INVALID;
+  }
   return embed_text(r, y_cond, static_cast<cudaStream_t>(stream));
 }
 
@@ -826,7 +831,9 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
     return DDIT_E_CONFIG;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  timed(r, K_EXCH, s, 1, [&] { return flag_wait(r->flags, r->counter + 1, r->g.P, s); });
+  timed(r, K_EXCH, s, 1, [&] {
+    return flag_wait(r->flags, r->counter + 1, r->g.P, r->counter + 2, s);
+  });
   return check_cuda("barrier");
 }
 
@@ -866,6 +873,26 @@ DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count) {
     count[r->ev_cls[i]] += 1;
   }
   r->ev_n = 0;
+  return DDIT_OK;
+}
+
+// counter[0] = exchange CTA tickets, [1] = exchange epoch, [2] = barrier status (0 = ok,
+// 1 + q = the wait on rank q's flag timed out: the group is broken)
+DDIT_API int ddit_request_status(ddit_req* r, void* stream, uint32_t* status) {
+  if (!r || !status) {
+    set_error("ddit_request_status: null argument");
+    return DDIT_E_INVALID;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t v = 0;
+  if (cudaMemcpyAsync(&v, r->counter + 2, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return check_cuda("ddit_request_status");
+  *status = v;
+  if (v) {
+    set_error("exchange barrier timed out waiting for rank %u of the group", v - 1);
+    return DDIT_E_CONFIG;
+  }
   return DDIT_OK;
 }
 

@@ -12,9 +12,10 @@ allocator / policy decision stays the reference's.
   A.6) the new group's ranks gather their new frame ranges from the old shards with
   ``ddit_latent_gather`` (peer loads) before the step -- the reference's 1 ms + 1 ms constants
   (engine.py:52-61) become a measured re-shard.
-* Engine GPU ids map onto physical devices ``gpu_id % device_count``. A group whose ids all
-  land on one device runs as virtual ranks in lockstep (``VirtualGroup``); a group spanning
-  devices runs one rank per device concurrently with the peer-store exchange.
+* Engine GPU ids map onto physical devices ``gpu_id % device_count``. A group whose ids land
+  on distinct devices runs one rank per device concurrently with the peer-store exchange; any
+  other group (all on one device, or more ranks than devices, e.g. DoP 4 on a 2-GPU box) runs
+  as virtual ranks in lockstep on the device of its first id (``VirtualGroup``).
 * Rank states (workspace, tables, GEMM / attention plans) are pooled per (resolution, devices):
   a new request re-binds a pooled group to its caption (``ddit_request_set_text``); a promotion
   takes a pooled group for the new GPU set and broadcasts the text state from the old rank 0
@@ -122,6 +123,12 @@ class B200Executor:
     def device_of(self, gpu_id: int) -> int:
         return gpu_id % self.ndev
 
+    def devices_of(self, gpu_ids: tuple[int, ...]) -> list[int]:
+        """Device of every rank of a group: one per id when the ids land on distinct devices,
+        else the whole group on the first id's device (virtual ranks)."""
+        devs = [self.device_of(g) for g in gpu_ids]
+        return devs if len(set(devs)) == len(devs) else [devs[0]] * len(devs)
+
     def _model(self, dev: int) -> STDiTModel:
         if dev not in self.models:
             self.models[dev] = STDiTModel(self.cfg, self._weights, torch.device("cuda", dev))
@@ -139,7 +146,7 @@ class B200Executor:
               text_from: StepRequest | None = None) -> _Live:
         """A group for ``gpu_ids``: pooled if one is idle (re-bound to this request's caption, or
         given ``text_from``'s text state by a broadcast copy), else newly opened."""
-        devs = [self.device_of(g) for g in gpu_ids]
+        devs = self.devices_of(gpu_ids)
         key = (request.resolution, tuple(devs))
         idle = self.pool.get(key)
         if idle:
@@ -157,7 +164,9 @@ class B200Executor:
     def _open_new(self, request: RequestState, gpu_ids: tuple[int, ...]) -> _Live:
         sh = self._shape(request)
         _, y = self._inputs(request)
-        devs = [self.device_of(g) for g in gpu_ids]
+        # more ranks than distinct devices (e.g. DoP 4 on a 2-GPU box): the whole group runs as
+        # virtual ranks on the device of its first id (emulate_group reports its P-GPU time)
+        devs = self.devices_of(gpu_ids)
         dop = len(gpu_ids)
         if len(set(devs)) == 1:
             model = self._model(devs[0])
@@ -166,8 +175,6 @@ class B200Executor:
                                    guidance=self.guidance)
             ranks, group = grp.ranks, grp
         else:
-            if len(set(devs)) != dop:
-                raise RuntimeError(f"group {gpu_ids} maps several ranks onto one device of many")
             ranks = []
             for r, d in enumerate(devs):
                 with torch.cuda.device(d):
@@ -286,8 +293,11 @@ class B200Executor:
         if q == 1 or self.vae_cfg is None:
             self.final_latents[request.request_id] = latents[0]
         else:  # the ranks' latent ranges overlap at micro-batch boundaries
-            zf = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
-            latent_gather(zf, 0, sh.T, srcs)
+            with torch.cuda.device(master):
+                zf = torch.empty((1, self.cfg.in_channels, *sh.latent), device=torch.device("cuda", master))
+                latent_gather(zf, 0, sh.T, srcs)
+                # the source shards go back to the pool below: finish reading them first
+                torch.cuda.current_stream().synchronize()
             self.final_latents[request.request_id] = zf
         self._close(live)
         if self.keep_videos and parts:
@@ -353,7 +363,10 @@ def profile_b200(cfg: STDiTConfig, weights: dict[str, torch.Tensor], labels: lis
     """Measure dit_step_seconds per (resolution, DoP) on this machine's GPUs and return a
     ``dit-profile/1`` document (reference profiles.py:132-215). DoPs beyond the visible device
     count run as virtual ranks on one device (flagged ``"virtual": true`` in the entry)."""
-    ex = B200Executor(cfg, weights)
+    # groups wider than the visible devices run as virtual ranks; emulate_group makes their
+    # entry the DoP-P latency (max over ranks + exchange bytes over NVLink), not the serialised
+    # time of all ranks on one device
+    ex = B200Executor(cfg, weights, emulate_group=True)
     entries = []
     for res in labels:
         for d in dops:

@@ -11,7 +11,8 @@ from .metrics import MetricsReport, compute_metrics, nearest_rank_percentile, no
 from .policies import (GreedyPolicy, PromoteEntry, SchedulingPolicy, StaticDopPolicy,
                        promotion_order, update_starvation)
 from .profiles import (DopTable, ProfileError, ProfileLookupError, ProfileTable, ResolutionClass,
-                       change_rate, derive_dop_table, dump_profiles, estimate_execution_time,
+                       change_rate, default_profile, derive_dop_table, dump_profiles,
+                       estimate_execution_time,
                        load_profiles, optimal_dop)
 from .workload import (ArrivalRecord, WorkloadError, WorkloadSpec, empirical_proportions,
                        generate, load_workload, save_workload, stratified_counts)

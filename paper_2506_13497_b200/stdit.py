@@ -197,6 +197,13 @@ class StepRequest:
                                                   ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def status(self, stream=None) -> int:
+        """Synchronise ``stream`` and raise if the group's exchange barrier timed out (a peer
+        never signalled); 0 when healthy."""
+        v = ctypes.c_uint32()
+        check(lib().ddit_request_status(self.handle, stream_ptr(stream), ctypes.byref(v)))
+        return v.value
+
     def set_option(self, option: int, value: int) -> None:
         check(lib().ddit_request_set_option(self.handle, option, value))
 

@@ -32,6 +32,18 @@ def test_default_profile_b_values():
     assert sched.derive_dop_table(t).by_resolution == {"144p": 1, "240p": 2, "360p": 4}
 
 
+def test_default_profile_matches_reference_bundle():
+    """sched.default_profile() == the reference's bundled document (ditsim.default_profile(),
+    reference profiles.py:291-300), recorded in the golden file."""
+    a = sched.default_profile()
+    b = sched.load_profiles(G["default_profile"])
+    assert a == b
+    assert sched.derive_dop_table(a).by_resolution == {"144p": 1, "240p": 2, "360p": 4}
+    # the 360p VAE share at DoP 4 is exactly 1/7 (reference test_profiles.py:170-173)
+    total = sched.estimate_execution_time(a, "360p", 4, 30)
+    assert abs(a.vae("360p") / total - 1 / 7) <= 1e-12
+
+
 def _handle(spec):
     return sched.AllocationHandle(tuple(sched.Block(s, o) for s, o in spec))
 
