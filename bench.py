@@ -9,7 +9,8 @@ after --warmup untimed ones, max over ranks. "e2e" is the same step through the 
 with the latent in pinned host memory (H2D of z and D2H of z' inside the timed region).
 
 Usage:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-        (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+        N > 1 runs one process per GPU: under torchrun (the driver's launch), or, when started
+        as a plain process, bench.py spawns the N ranks itself through torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -129,36 +130,89 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
-def cpu_reference_step_ms(label: str, samples: int = 1) -> tuple[float, dict]:
-    """fp32 torch-CPU restatement (oracle/stdit3.py) of the step on the host cores: a bounded
-    sample (the step at depth 1 = one spatial+temporal block pair, real 240p shape and XL/2
-    width), extrapolated to the 28-layer step by the FLOP ratio."""
-    from oracle import stdit3  # the checker / CPU baseline only
-    from paper_2506_13497_b200 import shapes, weights
+_ORACLE = {}
 
-    torch.set_num_threads(os.cpu_count() or 1)
-    cfg1 = dataclasses.replace(weights.XL2, depth=1)
-    sh = shapes.shape_of(label)
-    W = weights.init_weights(cfg1, seed=3)
-    z, y = weights.synthetic_inputs(cfg1, sh.latent)
-    times = []
+
+def _oracle_state(label: str):
+    """Weights / inputs of the CPU oracle for the full 28-layer XL/2 step (built once)."""
+    if label not in _ORACLE:
+        from oracle import stdit3  # the checker / CPU baseline only
+        from paper_2506_13497_b200 import shapes, weights
+
+        torch.set_num_threads(os.cpu_count() or 1)
+        cfg = weights.XL2
+        sh = shapes.shape_of(label)
+        W = weights.init_weights(cfg, seed=3)
+        z, y = weights.synthetic_inputs(cfg, sh.latent)
+        with torch.inference_mode():
+            text = stdit3.prepare_text(W, y)
+        _ORACLE[label] = (cfg, sh, W, z, text)
+    return _ORACLE[label]
+
+
+def cpu_reference_step_ms(label: str, step: int = 3) -> tuple[float, dict]:
+    """ONE real step of the fp32 torch-CPU restatement (oracle/stdit3.py) on the host cores:
+    STDiT3-XL/2, all 28 block pairs, the bench's shape, CFG batch 2 -- the same workload as the
+    GPU arm, timed (no extrapolation)."""
+    from oracle import stdit3
+
+    cfg, sh, W, z, text = _oracle_state(label)
     with torch.inference_mode():
-        y2 = stdit3.prepare_text(W, y)
-        for i in range(samples):
-            t0 = time.perf_counter()
-            stdit3.denoise_step(W, cfg1, z, y2, 3, sh.height, sh.width)
-            times.append(time.perf_counter() - t0)
-    t1 = min(times)
-    full = step_flops(weights.XL2, sh, include_text_kv=False)["total"]
-    part = step_flops(cfg1, sh, include_text_kv=False)["total"]
-    ms = t1 * (full / part) * 1e3
+        t0 = time.perf_counter()
+        stdit3.denoise_step(W, cfg, z, text, step, sh.height, sh.width)
+        ms = (time.perf_counter() - t0) * 1e3
     info = {
         "cores": torch.get_num_threads(),
-        "sample": (f"oracle fp32 torch-CPU denoise_step of {label}x51 XL/2 width at depth 1 "
-                   f"(one spatial+temporal block pair) timed {samples}x (min {t1:.2f} s), "
-                   f"scaled x{full / part:.1f} by FLOPs to the 28-layer step"),
+        "cpu": _cpu_model(),
+        "sample": (f"one full STDiT3-XL/2 denoise step (28 block pairs, {label} x 51, CFG batch 2) "
+                   "of the fp32 torch-CPU oracle port, timed end to end"),
     }
     return ms, info
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def sched_cpu_baseline() -> dict:
+    """SURVEY.md §8(d) CPU path (1): the scheduling loop itself -- the greedy step-granularity
+    allocator + serving engine (sched.Simulation + GreedyPolicy, the reference semantics
+    bit for bit) on BASELINE config 5's trace (48 requests, 1/3 each 144p/240p/360p, Poisson
+    rate 1.0, seed 0, 8 GPUs) in virtual time, fed the B200-measured profile. Host cost per
+    step event, single-threaded Python."""
+    from paper_2506_13497_b200 import sched
+
+    doc = None
+    f = ROOT / "profiles" / "r01_trace_replay_c5.json"
+    if f.exists():
+        try:
+            doc = json.loads(f.read_text())["profile"]
+        except Exception:
+            doc = None
+    table = sched.load_profiles(doc) if doc else sched.default_profile()
+    dt = sched.derive_dop_table(table)
+    spec = sched.WorkloadSpec(proportions={"144p": 1 / 3, "240p": 1 / 3, "360p": 1 / 3},
+                              total_requests=48, arrival_rate=1.0, seed=0)
+    best = None
+    for _ in range(5):
+        wl = sched.generate(spec)
+        t0 = time.perf_counter()
+        res = sched.Simulation(sched.ClusterTopology(1, 8), table, dt, wl, sched.GreedyPolicy(dt)).run()
+        el = time.perf_counter() - t0
+        best = el if best is None else min(best, el)
+    nstep = sum(1 for r in res.trace if r.kind == sched.EventKind.STEP_COMPLETE)
+    m = sched.compute_metrics(res)
+    return {"value": round(best / max(nstep, 1) * 1e6, 2), "unit": "us/step_event", "cores": 1,
+            "kind": "port", "step_events": nstep, "sim_seconds": round(best, 4),
+            "avg_latency_s": round(m.avg_latency, 4), "p99_latency_s": round(m.p99_latency, 4),
+            "profile": "B200-measured (profiles/r01_trace_replay_c5.json)" if doc else "default",
+            "sample": "config-5 trace, 48 requests, rate 1.0, seed 0, 1 node x 8 GPUs, best of 5"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -172,7 +226,7 @@ def run_ours(args) -> dict | None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (use torchrun for N>1)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     # one GPU per rank; on a box with fewer GPUs than ranks (a 1-GPU test box) the ranks share
     # devices round-robin and the plumbing falls back to gloo (NCCL needs a GPU per rank)
     ndev = torch.cuda.device_count()
@@ -344,24 +398,27 @@ def run_ours(args) -> dict | None:
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        cms, info = cpu_reference_step_ms(args.label, samples=1)
+        cms, info = cpu_reference_step_ms(args.label)
         out["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "kind": "port", **info}
+        out["cpu_baseline_sched"] = sched_cpu_baseline()
     return out
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args) -> dict | None:
     """The reference has no STDiT implementation (it looks the step time up,
-    reference pkg/src/ditsim/profiles.py:69-76); its CPU path is therefore the oracle port,
-    timed on the host cores on a bounded sample of the same workload."""
+    reference pkg/src/ditsim/profiles.py:69-76); its CPU implementation of the path is therefore
+    the oracle port (fp32 torch, every host core), run on the SAME workload as our arm: each of
+    the W + K steps is one full 28-layer XL/2 step at the bench shape (no extrapolation)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
     vals = []
     info = {}
+    t_start = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        ms, info = cpu_reference_step_ms(args.label, samples=1)
+        ms, info = cpu_reference_step_ms(args.label, step=(i % 30))
         if i >= args.warmup:
             vals.append(ms)
     v = sum(vals) / len(vals)
@@ -379,16 +436,34 @@ def run_reference(args) -> dict | None:
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded N(0,1) latent and caption embedding; random-init XL/2 weights)",
-        "config": {"workload": f"STDiT3-XL/2 denoise step, {args.label} x 51 frames, CFG batch 2 "
-                               "(fp32 CPU oracle port; the reference ships no model code)",
+        "config": {"workload": f"STDiT3-XL/2 denoise step, {args.label} x 51 frames (28 block pairs), "
+                               "CFG batch 2 (fp32 CPU oracle port; the reference ships no model code)",
                    "dop": 1},
-        "cpu_baseline": {"value": round(v, 1), "unit": "ms", "kind": "port", **info},
+        "cpu_baseline": {"value": round(v, 1), "unit": "ms", "kind": "port", **info,
+                         "min_ms": round(min(vals), 1), "max_ms": round(max(vals), 1)},
         "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_seconds": round(time.perf_counter() - t_start, 1),
     }
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: launch the N ranks ourselves (one process per GPU, the same
+    command the driver uses) and pass rank 0's JSON line through."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     out = run_reference(args) if args.impl == "reference" else run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)

@@ -126,8 +126,10 @@ def self_attention(W, p, cfg, x, rope: bool):
         pos = torch.arange(L)
         q = rope_interleaved(q, pos)
         k = rope_interleaved(k, pos)
-    attn = (q * D**-0.5) @ k.transpose(-2, -1)
-    o = attn.softmax(-1) @ v
+    # sequences in chunks so the fp32 score matrix stays <= ~1 GB (720p: L = 3600 tokens)
+    step = max(1, (1 << 28) // (H * L * L))
+    o = torch.cat([((q[i:i + step] * D**-0.5) @ k[i:i + step].transpose(-2, -1)).softmax(-1)
+                   @ v[i:i + step] for i in range(0, Bq, step)], 0)
     o = o.transpose(1, 2).reshape(Bq, L, C)
     return F.linear(o, W[p + "attn.proj.weight"], W[p + "attn.proj.bias"])
 

@@ -16,7 +16,8 @@ def ref_attn(q, k, v):  # [n, L, H, D]
 
 
 @pytest.mark.parametrize("tc", [False, True])
-@pytest.mark.parametrize("B,T,S", [(2, 3, 405), (2, 1, 64), (1, 2, 130), (2, 4, 1), (2, 2, 920), (1, 1, 1620), (1, 3, 256)])
+@pytest.mark.parametrize("B,T,S", [(2, 3, 405), (2, 1, 64), (1, 2, 130), (2, 4, 1), (2, 2, 920), (1, 1, 1620), (1, 3, 256),
+                                   (2, 1, 3600), (1, 2, 3600)])
 def test_spatial(cuda, B, T, S, tc):
     from paper_2506_13497_b200 import kernels
     g = torch.Generator().manual_seed(0)
@@ -28,11 +29,14 @@ def test_spatial(cuda, B, T, S, tc):
                       Lq=S, Lk=S, q_map=(1, S, 0, 1), kv_map=(1, S, 0, 1), tc=tc)
     q, k, v = qkv.view(B * T, S, 3, H, D).unbind(2)
     ref = ref_attn(q, k, v).reshape(M, C)
-    assert rel_l2(o, ref) < 1e-2
+    e = rel_l2(o, ref)
+    print(f"spatial B={B} T={T} S={S} tc={tc}: relL2 {e:.2e}")
+    assert e < 1e-2
 
 
 @pytest.mark.parametrize("fast", [False, True])
-@pytest.mark.parametrize("B,T,Sl", [(2, 15, 405), (2, 30, 17), (1, 4, 3), (2, 70, 5), (2, 16, 9), (1, 32, 2), (2, 1, 3)])
+@pytest.mark.parametrize("B,T,Sl", [(2, 15, 405), (2, 30, 17), (1, 4, 3), (2, 70, 5), (2, 16, 9), (1, 32, 2), (2, 1, 3),
+                                    (2, 30, 450)])
 def test_temporal(cuda, B, T, Sl, fast):
     if fast and T > 32:
         pytest.skip("short-sequence kernel is for T <= 32")
@@ -48,7 +52,9 @@ def test_temporal(cuda, B, T, Sl, fast):
     x = qkv.view(B, T, Sl, 3, H, D).transpose(1, 2).reshape(B * Sl, T, 3, H, D)
     q, k, v = x.unbind(2)
     ref = ref_attn(q, k, v).reshape(B, Sl, T, C).transpose(1, 2).reshape(M, C)
-    assert rel_l2(o, ref) < 1e-2
+    e = rel_l2(o, ref)
+    print(f"temporal B={B} T={T} Sl={Sl} fast={fast}: relL2 {e:.2e}")
+    assert e < 1e-2
 
 
 @pytest.mark.parametrize("tc", [False, True])
