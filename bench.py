@@ -44,6 +44,10 @@ def parse() -> argparse.Namespace:
     ap.add_argument("--label", default=LABEL)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly, no CUDA graph")
+    ap.add_argument("--xch", default="fused", choices=["fused", "kernel", "nccl"],
+                    help="DoP > 1 all-to-all: fused into the fc2 GEMM epilogue (peer stores, "
+                         "default), the stand-alone peer-store kernel, or packed rows through "
+                         "ncclAllToAll (the baseline arm)")
     return ap.parse_args()
 
 
@@ -233,8 +237,12 @@ def run_ours(args) -> dict | None:
     dev = torch.device("cuda", local % ndev)
     torch.cuda.set_device(dev)
     shared_gpus = world > ndev
+    if args.xch == "kernel":
+        os.environ["DDIT_FUSED_XCH"] = "0"
     if world > 1:
         if shared_gpus:
+            if args.xch == "nccl":
+                raise SystemExit("--xch nccl needs one GPU per rank (NCCL rejects shared devices)")
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
@@ -246,7 +254,13 @@ def run_ours(args) -> dict | None:
     del W
     torch.cuda.empty_cache()
     z_full, y = weights.synthetic_inputs(cfg, sh.latent, device=dev)
-    if world > 1:
+    grp = None
+    if world > 1 and args.xch == "nccl":
+        from paper_2506_13497_b200.dist import NcclGroupStep
+
+        grp = NcclGroupStep(model, sh, y)
+        req = grp.req
+    elif world > 1:
         from paper_2506_13497_b200.dist import GroupStep
 
         grp = GroupStep(model, sh, y)
@@ -262,10 +276,11 @@ def run_ours(args) -> dict | None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    use_graph = not args.no_graph
-    run_step = req.graph_step if use_graph else req.step
+    nccl = world > 1 and args.xch == "nccl"
+    use_graph = not args.no_graph and not nccl  # the NCCL arm launches eagerly
+    run_step = grp.step if nccl else (req.graph_step if use_graph else req.step)
     for i in range(args.warmup):
-        req.step(z, i % 30)
+        run_step(z, i % 30) if nccl else req.step(z, i % 30)
     if use_graph:  # capture every step index the timed loops use (outside the timed region)
         for i in range(args.steps):
             run_step(z, (args.warmup + i) % 30)
@@ -284,6 +299,8 @@ def run_ours(args) -> dict | None:
     e1.record(stream)
     barrier()
     launches = launch_count() - launches0
+    if world > 1:
+        req.status()  # raises if a peer never signalled (bounded barrier spin)
     if use_graph:  # graph replays do not pass through the launch counter: count one step
         l0 = launch_count()
         req.step(z, 0)
@@ -294,15 +311,21 @@ def run_ours(args) -> dict | None:
     # ---- the same K steps again with an event pair around every launch (roofline evidence:
     # per-kernel-class device time on the launching stream)
     req.profile(True)
+    if nccl:
+        grp.timing = True
+        grp.read_timing()
     barrier()
     e0.record(stream)
     for i in range(args.steps):
-        req.step(z, (args.warmup + i) % 30)
+        (grp.step if nccl else req.step)(z, (args.warmup + i) % 30)
     e1.record(stream)
     barrier()
     ms_total = e0.elapsed_time(e1)
     prof = req.profile_read()
     req.profile(False)
+    a2a_ms = grp.read_timing() / args.steps if nccl else None
+    if nccl:
+        grp.timing = False
     clk = clocks.stop()
 
     # ---- e2e: through the public step API with the latent in pinned host memory
@@ -318,6 +341,11 @@ def run_ours(args) -> dict | None:
     e2e_ms = e0.elapsed_time(e1) / args.steps
     zbytes = z.numel() * 4
 
+    if world > 1:
+        from paper_2506_13497_b200.executor import exchange_bytes
+
+        xb = exchange_bytes(sh, world, rank, cfg.hidden)
+        xfer_ms = a2a_ms if nccl else prof["exchange"][0] / args.steps
     cdev = torch.device("cpu") if shared_gpus else dev
     t_step = torch.tensor([ms_step, e2e_ms], device=cdev)
     if world > 1:
@@ -364,7 +392,10 @@ def run_ours(args) -> dict | None:
                         f"(latent {sh.T}x{sh.latent[1]}x{sh.latent[2]}, {sh.N} tokens/sample), "
                         "CFG batch 2, RFLOW Euler update",
             "dop": world,
-            "parallelism": (f"sp{world} (DSP T-shard/S-shard all-to-all, fused into the fc2 GEMM)"
+            "parallelism": (f"sp{world} (DSP T-shard/S-shard all-to-all: "
+                            + {"fused": "fused into the fc2 GEMM epilogue as peer stores",
+                               "kernel": "stand-alone peer-store exchange kernel",
+                               "nccl": "packed rows through ncclAllToAll"}[args.xch] + ")"
                             + (f"; {world} ranks sharing {ndev} GPU(s): not a scaling number"
                                if shared_gpus else "")) if world > 1 else "none",
             "step_tflop": round(fl["total"] / 1e12, 3),
@@ -397,6 +428,20 @@ def run_ours(args) -> dict | None:
         "breakdown_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in prof.items()},
         "clocks": clk,
     }
+    if world > 1:
+        xi = {"mode": args.xch, "bytes_per_rank_per_step": xb,
+              "exchanges_per_step": 2 * cfg.depth, "row_dtype": "f32"}
+        if nccl:
+            xi.update({"a2a_ms_per_step_rank0": round(xfer_ms, 3),
+                       "nvlink_gbs_rank0": round(xb / (xfer_ms * 1e-3) / 1e9, 1) if xfer_ms else None,
+                       "how": "CUDA events around every all_to_all_single on rank 0"})
+        else:
+            xi.update({"barrier_wait_ms_per_step_rank0": round(xfer_ms, 3),
+                       "how": "rows stored into peer memory by the fc2 epilogue (fused) or the "
+                              "exchange kernel; the listed time is the flag-barrier wait"})
+        if shared_gpus:
+            xi["note"] = "ranks share one GPU: peer stores are local, no NVLink figure"
+        out["exchange"] = xi
     if world == 1 and not args.no_cpu_baseline:
         cms, info = cpu_reference_step_ms(args.label)
         out["cpu_baseline"] = {"value": round(cms, 1), "unit": "ms", "kind": "port", **info}

@@ -201,6 +201,21 @@ DDIT_API int ddit_request_set_text(ddit_req* r, const float* y_cond, void* strea
  * copy src's text embedding and cross-attention K/V cache into dst (same model; dst may live on
  * another peer-enabled device -- the copy then crosses NVLink). */
 DDIT_API int ddit_request_copy_text(ddit_req* dst, const ddit_req* src, void* stream);
+/* Cheaper promotion broadcast: copy only src's y-embedding (B*300 x C bf16) into dst and
+ * recompute the 2*depth cross-attention K/V projections on dst's device (same result bit for bit
+ * as ddit_request_copy_text; per new rank 1.4 MB over NVLink + 56 small GEMMs instead of 155 MB). */
+DDIT_API int ddit_request_share_text(ddit_req* dst, const ddit_req* src, void* stream);
+/* Promotion P -> P' for a whole new group in one call (SURVEY §8(b) ddit_reshard): rank i of the
+ * new group (new_ranks[i], its z shard new_z[i], on its own device / streams[i] or the legacy
+ * stream when streams is NULL) gathers its frames [t_lo, t_hi) from the p old shards old_z[k]
+ * (frames [old_t_lo[k], old_t_hi[k]), peer pointers) and takes its text state from text_src
+ * (ddit_request_share_text). Replaces OverheadModel.broadcast_seconds + scale_up_seconds
+ * (reference engine.py:52-61, applied at :281-290). */
+DDIT_API int ddit_reshard(ddit_req* const* new_ranks, float* const* new_z, int q,
+                          const float* const* old_z, const int* old_t_lo, const int* old_t_hi,
+                          int p, const ddit_req* text_src, void* const* streams);
+/* Device ms of the last ddit_reshard work into rank r (synchronises on it). */
+DDIT_API int ddit_request_reshard_ms(ddit_req* r, float* ms);
 
 /* DoP > 1: register every rank's exchange buffers (x_sp, x_tp: fp32, as returned by
  * ddit_request_exchange_buffers on that rank, peer-mapped) and flag arrays (uint32 [P]). */
@@ -224,6 +239,8 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream);
  * bounded (env DDIT_XCH_TIMEOUT_MS, default 20000); status = 0 ok, or 1 + the rank whose flag
  * never arrived, returned with DDIT_E_CONFIG. */
 DDIT_API int ddit_request_status(ddit_req* r, void* stream, uint32_t* status);
+/* Bound of the barrier spin in ms for launches from now on (<= 0: DDIT_XCH_TIMEOUT_MS / 20 s). */
+DDIT_API int ddit_set_exchange_timeout_ms(int ms);
 
 /* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
@@ -231,12 +248,26 @@ DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float*
 /* Request options: DDIT_OPT_TC_ATTENTION (default 1) selects the tcgen05 FMHA for spatial /
  * cross attention; 0 falls back to the mma.sync flash kernel (kept as the baseline). */
 #define DDIT_OPT_TC_ATTENTION 1
+/* DDIT_OPT_EXTERNAL_XCH (default 0): the step does not exchange rows itself (no peers, no fused
+ * fc2 stores, no flag barrier); after every ddit_step_phase the caller moves them with
+ * ddit_request_xch_pack -> an all-to-all (ncclAllToAll in dist.NcclGroupStep) ->
+ * ddit_request_xch_unpack. The baseline the fused peer-store exchange is measured against. */
+#define DDIT_OPT_EXTERNAL_XCH 2
 DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value);
 
 /* Profiling: while enabled every launch of the request is bracketed by CUDA events on its
  * stream; _read returns per-class totals (ms, launches) for classes
  * 0 = tcgen05 GEMM, 1 = attention, 2 = elementwise / embed / final, 3 = exchange + barrier,
  * and resets. */
+/* Staged all-to-all after phase `phase` (even: spatial block, x_sp -> x_tp; odd: temporal,
+ * x_tp -> x_sp). Rows are C fp32. xch_counts: rows this rank sends to / receives from every
+ * rank q (arrays of dop ints). xch_pack writes the rows into `send` grouped by destination rank
+ * (contiguous, rank order); xch_unpack scatters `recv` (grouped by source rank) into the other
+ * layout. Replaces the paper's NCCL all-to-all between sequence-parallel workers
+ * (reference engine.py:286-290 only charges a constant). */
+DDIT_API int ddit_request_xch_counts(ddit_req* r, int phase, int* send_rows, int* recv_rows);
+DDIT_API int ddit_request_xch_pack(ddit_req* r, int phase, void* send, void* stream);
+DDIT_API int ddit_request_xch_unpack(ddit_req* r, int phase, const void* recv, void* stream);
 DDIT_API int ddit_request_profile(ddit_req* r, int enable);
 DDIT_API int ddit_request_profile_read(ddit_req* r, float* ms, int* count);
 /* Total kernel launches issued by libddit in this process. */

@@ -128,6 +128,7 @@ _SIGNATURES = {
     "ddit_set_gemm_2cta": [ci],
     "ddit_set_pdl": [ci],
     "ddit_set_fused_exchange": [ci],
+    "ddit_set_exchange_timeout_ms": [ci],
     "ddit_enable_peer_access": [ci, ci],
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
@@ -139,6 +140,10 @@ _SIGNATURES = {
                           ctypes.POINTER(vp)],
     "ddit_request_set_text": [vp, vp, vp],
     "ddit_request_copy_text": [vp, vp, vp],
+    "ddit_request_share_text": [vp, vp, vp],
+    "ddit_reshard": [ctypes.POINTER(vp), ctypes.POINTER(vp), ci, ctypes.POINTER(vp),
+                     ctypes.POINTER(ci), ctypes.POINTER(ci), ci, vp, ctypes.POINTER(vp)],
+    "ddit_request_reshard_ms": [vp, ctypes.POINTER(cf)],
     "ddit_request_exchange_buffers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "ddit_request_set_peers": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)],
     "ddit_dit_step": [vp, vp, ci, vp],
@@ -149,6 +154,9 @@ _SIGNATURES = {
     "ddit_request_status": [vp, vp, ctypes.POINTER(ctypes.c_uint32)],
     "ddit_request_timestep": [vp, ci, ctypes.POINTER(cf), ctypes.POINTER(cf)],
     "ddit_request_profile": [vp, ci],
+    "ddit_request_xch_counts": [vp, ci, ctypes.POINTER(ci), ctypes.POINTER(ci)],
+    "ddit_request_xch_pack": [vp, ci, vp, vp],
+    "ddit_request_xch_unpack": [vp, ci, vp, vp],
     "ddit_request_set_option": [vp, ci, ci],
     "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
     "ddit_conv": [ctypes.POINTER(ConvArgs), vp],

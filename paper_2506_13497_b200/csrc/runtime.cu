@@ -39,6 +39,10 @@ struct ddit_model {
   ddit_weights w;
   std::vector<ddit_block_weights> blocks;
   const float** sst_dev = nullptr;  // device array of 2*depth scale_shift_table pointers
+  // every block's cross-attention K/V projection stacked into one [2*depth*2C, C] matrix (+ bias)
+  // so a request's whole K/V cache is ONE GEMM (M = B*300, N = 2*depth*2C = 129024 at XL/2)
+  bf16* ckv_all = nullptr;
+  float* ckv_b_all = nullptr;
 };
 
 namespace {
@@ -145,6 +149,7 @@ struct ddit_req {
   unsigned int* counter;
   std::vector<float> ts;  // transformed timesteps
   std::vector<GemmPlan> plans;  // [2*depth][G_N]
+  std::vector<GemmPlan> text_plans;  // y_embedder fc1, fc2, then the 2*depth cross K/V GEMMs
   std::vector<FmhaPlan> fm_self;   // [2*depth] tcgen05 self-attention plans (spatial blocks)
   std::vector<FmhaPlan> fm_cross;  // [2*depth] tcgen05 cross-attention plans
   std::vector<uint8_t> fm_self_ok, fm_cross_ok;
@@ -154,13 +159,18 @@ struct ddit_req {
   bool flags_set = false;
   bool use_tc_attention = true;  // tcgen05 FMHA for spatial / cross attention
   bool fused_xch = false;        // the fc2 GEMM of every block performs the DSP exchange
+  bool external_xch = false;     // the caller moves the rows (staged pack -> ncclAllToAll -> unpack)
   // profiling: event pairs around every launch, tagged by kernel class
   bool prof_on = false;
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_cls;
   size_t ev_n = 0;
+  int device = 0;                           // the GPU this rank state lives on
+  cudaEvent_t rs0 = nullptr, rs1 = nullptr;  // timing of the last re-shard into this rank
   ~ddit_req() {
     for (auto e : ev) cudaEventDestroy(e);
+    if (rs0) cudaEventDestroy(rs0);
+    if (rs1) cudaEventDestroy(rs1);
   }
 };
 
@@ -394,14 +404,15 @@ ddit_attn cross_attn_args(const ddit_req* r, int k) {
   const int C = c.hidden;
   const int M = (k & 1) ? g.M_tp : g.M_sp;
   const int rpb = M / g.B;
-  const bf16* kv = r->kv + (size_t)k * g.B * c.text_tokens * 2 * C;
+  // kv [B*300][2*depth][2C]: block k's K at column 2Ck, its V at 2Ck + C
+  const bf16* kv = r->kv + (size_t)k * 2 * C;
   ddit_attn a;
   memset(&a, 0, sizeof a);
   a.q = r->xm;
   a.ldq = C;
   a.k = kv;
   a.v = kv + C;
-  a.ldk = a.ldv = 2 * C;
+  a.ldk = a.ldv = 2 * c.depth * 2 * C;
   a.o = r->ao;
   a.ldo = C;
   a.heads = c.heads;
@@ -480,7 +491,7 @@ int run_block(ddit_req* r, int k, cudaStream_t s) {
 
 int push_exchange(ddit_req* r, int k, cudaStream_t s) {
   const Geometry& g = r->g;
-  if (g.P == 1) return DDIT_OK;
+  if (g.P == 1 || r->external_xch) return DDIT_OK;
   // fused: the block's fc2 GEMM already stored its rows at their owners and signalled (a rank
   // without rows in this layout runs no GEMM, so it still signals through the exchange kernel)
   if (r->fused_xch && ((k & 1) ? g.M_tp : g.M_sp) > 0) return DDIT_OK;
@@ -536,7 +547,21 @@ DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, dd
       cudaMemcpy(m->sst_dev, sst.data(), sst.size() * sizeof(float*), cudaMemcpyHostToDevice) !=
           cudaSuccess) {
     set_error("ddit_model_create: cudaMalloc failed");
-    delete m;
+    ddit_model_destroy(m);
+    return DDIT_E_ALLOC;
+  }
+  // stacked cross-attention K/V weights (a device-side copy; the caller's tensors stay theirs)
+  const size_t kvw = (size_t)2 * cfg->hidden * cfg->hidden, kvb = (size_t)2 * cfg->hidden;
+  bool ok = cudaMalloc(&m->ckv_all, 2 * cfg->depth * kvw * sizeof(bf16)) == cudaSuccess &&
+            cudaMalloc(&m->ckv_b_all, 2 * cfg->depth * kvb * sizeof(float)) == cudaSuccess;
+  for (int k = 0; ok && k < 2 * cfg->depth; ++k)
+    ok = cudaMemcpy(m->ckv_all + k * kvw, m->blocks[k].ckv_w, kvw * sizeof(bf16),
+                    cudaMemcpyDeviceToDevice) == cudaSuccess &&
+         cudaMemcpy(m->ckv_b_all + k * kvb, m->blocks[k].ckv_b, kvb * sizeof(float),
+                    cudaMemcpyDeviceToDevice) == cudaSuccess;
+  if (!ok) {
+    set_error("ddit_model_create: stacked K/V weights: %s", cudaGetErrorString(cudaGetLastError()));
+    ddit_model_destroy(m);
     return DDIT_E_ALLOC;
   }
   *out = m;
@@ -546,6 +571,8 @@ DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, dd
 DDIT_API void ddit_model_destroy(ddit_model* m) {
   if (!m) return;
   cudaFree(m->sst_dev);
+  cudaFree(m->ckv_all);
+  cudaFree(m->ckv_b_all);
   delete m;
 }
 
@@ -574,51 +601,71 @@ DDIT_API int ddit_request_shard(const ddit_model* m, const ddit_req_desc* d, int
 
 // Caption -> per-request text state: [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb
 // [B*300, C], then the per-block cross-attention K/V cache kv[k] = yemb . Wkv^T + b.
-static int embed_text(ddit_req* r, const float* y_cond, cudaStream_t s) {
+// The 2 + 2*depth GEMM plans (fixed buffers of the request) are built once per request, so
+// re-binding a pooled request or rebuilding the K/V cache after a promotion costs only launches.
+static int text_plans(ddit_req* r) {
+  if (!r->text_plans.empty()) return DDIT_OK;
   const ddit_model* m = r->m;
   const ddit_config& c = m->cfg;
-  const Geometry& g = r->g;
-  int rc;
-  // [y_cond; y_null] -> bf16 -> y_embedder MLP -> yemb [B*300, C]
-  const int Ly = g.B * c.text_tokens;
-  const size_t ycount = (size_t)c.text_tokens * c.caption_channels;
+  const int Ly = r->g.B * c.text_tokens;
   bf16* ycat = r->big;
   bf16* yhid = r->big + (size_t)Ly * c.caption_channels;
-  cast_bf16(y_cond, ycat, ycount, s);
-  cast_bf16(m->w.y_null, ycat + ycount, ycount, s);
-  GemmPlan gp;
+  std::vector<GemmPlan> tp(3);
   EpiParams e;
   memset(&e, 0, sizeof e);
   e.bias = m->w.y1_b;
   e.out = yhid;
   e.ldo = c.hidden;
-  if ((rc = gemm_plan_init(&gp, ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly,
-                           c.hidden, c.caption_channels, EPI_GELU_BF16, e, pick_bn(c.hidden))) ||
-      (rc = launch(gp, s))) {
-    set_error("y_embedder fc1: %s", gemm_last_error());
-    return DDIT_E_CUDA;
+  if (gemm_plan_init(&tp[0], ycat, c.caption_channels, m->w.y1_w, c.caption_channels, Ly, c.hidden,
+                     c.caption_channels, EPI_GELU_BF16, e, pick_bn(c.hidden))) {
+    set_error("y_embedder fc1 plan: %s", gemm_last_error());
+    return DDIT_E_INVALID;
   }
   e.bias = m->w.y2_b;
   e.out = r->yemb;
-  if ((rc = gemm_plan_init(&gp, yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden,
-                           EPI_BF16, e, pick_bn(c.hidden))) ||
-      (rc = launch(gp, s))) {
-    set_error("y_embedder fc2: %s", gemm_last_error());
-    return DDIT_E_CUDA;
+  if (gemm_plan_init(&tp[1], yhid, c.hidden, m->w.y2_w, c.hidden, Ly, c.hidden, c.hidden, EPI_BF16,
+                     e, pick_bn(c.hidden))) {
+    set_error("y_embedder fc2 plan: %s", gemm_last_error());
+    return DDIT_E_INVALID;
   }
-  // per-block cross-attention K/V cache: kv[k] = yemb . Wkv^T + b  [B*300, 2C]
-  for (int k = 0; k < 2 * c.depth; ++k) {
-    memset(&e, 0, sizeof e);
-    e.bias = m->blocks[k].ckv_b;
-    e.out = r->kv + (size_t)k * Ly * 2 * c.hidden;
-    e.ldo = 2 * c.hidden;
-    if ((rc = gemm_plan_init(&gp, r->yemb, c.hidden, m->blocks[k].ckv_w, c.hidden, Ly,
-                             2 * c.hidden, c.hidden, EPI_BF16, e, pick_bn(2 * c.hidden))) ||
-        (rc = launch(gp, s))) {
-      set_error("cross kv: %s", gemm_last_error());
-      return DDIT_E_CUDA;  // r stays owned by the caller (ddit_request_open frees it on failure)
-    }
+  // all blocks' K/V in one GEMM: kv [Ly][2*depth*2C] = yemb . ckv_all^T + ckv_b_all
+  const int nkv = 2 * c.depth * 2 * c.hidden;
+  memset(&e, 0, sizeof e);
+  e.bias = m->ckv_b_all;
+  e.out = r->kv;
+  e.ldo = nkv;
+  int bn = 0, two = 0;
+  gemm_pick_tile(Ly, nkv, EPI_BF16, &bn, &two);
+  if (gemm_plan_init_cta(&tp[2], r->yemb, c.hidden, m->ckv_all, c.hidden, Ly, nkv, c.hidden,
+                         EPI_BF16, e, bn, two)) {
+    set_error("cross kv plan: %s", gemm_last_error());
+    return DDIT_E_INVALID;
   }
+  r->text_plans.swap(tp);
+  return DDIT_OK;
+}
+
+// per-block cross-attention K/V cache from the request's yemb
+static int cross_kv(ddit_req* r, cudaStream_t s) {
+  int rc = text_plans(r);
+  if (rc) return rc;
+  if ((rc = launch(r->text_plans[2], s))) return rc;
+  g_launches += 1;
+  return DDIT_OK;
+}
+
+static int embed_text(ddit_req* r, const float* y_cond, cudaStream_t s) {
+  const ddit_model* m = r->m;
+  const ddit_config& c = m->cfg;
+  int rc = text_plans(r);
+  if (rc) return rc;
+  const size_t ycount = (size_t)c.text_tokens * c.caption_channels;
+  bf16* ycat = r->big;
+  cast_bf16(y_cond, ycat, ycount, s);
+  cast_bf16(m->w.y_null, ycat + ycount, ycount, s);
+  if ((rc = launch(r->text_plans[0], s)) || (rc = launch(r->text_plans[1], s))) return rc;
+  g_launches += 4;
+  if ((rc = cross_kv(r, s))) return rc;
   return check_cuda("embed_text");
 }
 
@@ -629,6 +676,7 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   if (!r) return DDIT_E_ALLOC;
   r->m = m;
   r->d = *d;
+  cudaGetDevice(&r->device);
   int rc = geometry(m->cfg, *d, &r->g);
   if (rc) {
     delete r;
@@ -729,6 +777,78 @@ DDIT_API int ddit_request_copy_text(ddit_req* dst, const ddit_req* src, void* st
   cudaMemcpyAsync(dst->yemb, src->yemb, Ly * c.hidden * 2, cudaMemcpyDefault, s);
   cudaMemcpyAsync(dst->kv, src->kv, (size_t)2 * c.depth * Ly * 2 * c.hidden * 2, cudaMemcpyDefault, s);
   return check_cuda("ddit_request_copy_text");
+}
+
+// Promotion-time text state for a new rank: only the y-embedding (B*300 x C bf16, 1.4 MB at XL/2)
+// crosses from src (a peer copy when src is on another device); the 2*depth cross-attention K/V
+// projections are recomputed on dst's own GPU (bit-identical: same kernels, same inputs), so a
+// 1 -> 8 promotion does not push 8 x 155 MB of K/V cache out of one GPU.
+DDIT_API int ddit_request_share_text(ddit_req* dst, const ddit_req* src, void* stream) {
+  if (!dst || !src) {
+    set_error("ddit_request_share_text: null argument");
+    return DDIT_E_INVALID;
+  }
+  const ddit_config& c = dst->m->cfg;
+  if (src->m->cfg.hidden != c.hidden || src->m->cfg.depth != c.depth ||
+      src->m->cfg.text_tokens != c.text_tokens || src->g.B != dst->g.B) {
+    set_error("share_text: requests of different models");
+    return DDIT_E_CONFIG;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t Ly = (size_t)dst->g.B * c.text_tokens;
+  if (dst->yemb != src->yemb &&
+      cudaMemcpyAsync(dst->yemb, src->yemb, Ly * c.hidden * 2, cudaMemcpyDefault, s) != cudaSuccess)
+    return check_cuda("share_text copy");
+  int rc = cross_kv(dst, s);
+  if (rc) return rc;
+  return check_cuda("ddit_request_share_text");
+}
+
+// Promotion P -> P' in one call (SURVEY.md §8(b) `ddit_reshard`; reference engine.py:281-290
+// charges OverheadModel's 1 ms broadcast + 1 ms scale-up): for every rank i of the new group, on
+// its own device and stream, gather its new T-shard of z from the old group's shards (peer
+// loads) and take the text state from text_src (ddit_request_share_text). Host cost is one call
+// for the whole group; each new rank records start / end events (ddit_request_reshard_ms).
+DDIT_API int ddit_reshard(ddit_req* const* new_ranks, float* const* new_z, int q,
+                          const float* const* old_z, const int* old_t_lo, const int* old_t_hi,
+                          int p, const ddit_req* text_src, void* const* streams) {
+  if (!new_ranks || !new_z || !old_z || !old_t_lo || !old_t_hi || !text_src || q < 1 ||
+      q > kMaxDop || p < 1 || p > kMaxDop) {
+    set_error("ddit_reshard: bad arguments");
+    return DDIT_E_INVALID;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  int rc = DDIT_OK;
+  for (int i = 0; i < q && rc == DDIT_OK; ++i) {
+    ddit_req* r = new_ranks[i];
+    cudaStream_t s = streams ? static_cast<cudaStream_t>(streams[i]) : nullptr;
+    cudaSetDevice(r->device);
+    if (!r->rs0 && (cudaEventCreate(&r->rs0) != cudaSuccess || cudaEventCreate(&r->rs1) != cudaSuccess)) {
+      rc = check_cuda("reshard events");
+      break;
+    }
+    cudaEventRecord(r->rs0, s);
+    const ddit_config& c = r->m->cfg;
+    rc = ddit_latent_gather(new_z[i], r->g.t_lo, r->g.t_hi, old_z, old_t_lo, old_t_hi, p,
+                            c.in_channels, r->g.Hl * r->g.Wl, s);
+    if (rc == DDIT_OK && r != text_src) rc = ddit_request_share_text(r, text_src, s);
+    cudaEventRecord(r->rs1, s);
+    g_launches += 1;
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+DDIT_API int ddit_request_reshard_ms(ddit_req* r, float* ms) {
+  if (!r || !ms || !r->rs0) {
+    set_error("ddit_request_reshard_ms: no re-shard recorded");
+    return DDIT_E_INVALID;
+  }
+  if (cudaEventSynchronize(r->rs1) != cudaSuccess ||
+      cudaEventElapsedTime(ms, r->rs0, r->rs1) != cudaSuccess)
+    return check_cuda("ddit_request_reshard_ms");
+  return DDIT_OK;
 }
 
 DDIT_API int ddit_request_exchange_buffers(ddit_req* r, void** x_sp, void** x_tp, void** flags) {
@@ -837,6 +957,11 @@ DDIT_API int ddit_step_barrier(ddit_req* r, void* stream) {
   return check_cuda("barrier");
 }
 
+DDIT_API int ddit_set_exchange_timeout_ms(int ms) {
+  set_flag_timeout_ms(ms);
+  return DDIT_OK;
+}
+
 DDIT_API int ddit_set_fused_exchange(int on) {
   g_fused_xch = on ? 1 : 0;
   return DDIT_OK;
@@ -847,9 +972,75 @@ DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value) {
     case DDIT_OPT_TC_ATTENTION:
       r->use_tc_attention = value != 0;
       return DDIT_OK;
+    case DDIT_OPT_EXTERNAL_XCH:
+      r->external_xch = value != 0;
+      return DDIT_OK;
   }
   set_error("unknown option %d", option);
   return DDIT_E_INVALID;
+}
+
+// ---- staged all-to-all for an external collective (the NCCL arm, DDIT_OPT_EXTERNAL_XCH)
+static XchGeom xch_geom(const ddit_req* r) {
+  const Geometry& g = r->g;
+  XchGeom x;
+  x.B = g.B;
+  x.T = g.T;
+  x.S = g.S;
+  x.C = r->m->cfg.hidden;
+  x.P = g.P;
+  x.Tl = g.Tl;
+  x.Sl = g.Sl;
+  return x;
+}
+
+DDIT_API int ddit_request_xch_counts(ddit_req* r, int phase, int* send_rows, int* recv_rows) {
+  if (!r || !send_rows || !recv_rows || phase < 0 || phase >= 2 * r->m->cfg.depth) {
+    set_error("ddit_request_xch_counts: bad argument");
+    return DDIT_E_INVALID;
+  }
+  xch_counts(xch_geom(r), phase & 1, send_rows, recv_rows);
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_request_xch_pack(ddit_req* r, int phase, void* send, void* stream) {
+  if (!r || phase < 0 || phase >= 2 * r->m->cfg.depth) {
+    set_error("ddit_request_xch_pack: bad argument");
+    return DDIT_E_INVALID;
+  }
+  const XchGeom x = xch_geom(r);
+  const int dir = phase & 1;
+  int sr[kMaxDop], rr[kMaxDop], rows = 0;
+  xch_counts(x, dir, sr, rr);
+  for (int q = 0; q < x.P; ++q) rows += sr[q];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int n = 0;
+  timed(r, K_EXCH, s, 0, [&] {
+    n = xch_pack(dir == 0 ? r->x_sp : r->x_tp, static_cast<float*>(send), x, dir, rows, s);
+    return 0;
+  });
+  g_launches += (unsigned long long)n;
+  return check_cuda("xch_pack");
+}
+
+DDIT_API int ddit_request_xch_unpack(ddit_req* r, int phase, const void* recv, void* stream) {
+  if (!r || phase < 0 || phase >= 2 * r->m->cfg.depth) {
+    set_error("ddit_request_xch_unpack: bad argument");
+    return DDIT_E_INVALID;
+  }
+  const XchGeom x = xch_geom(r);
+  const int dir = phase & 1;
+  int sr[kMaxDop], rr[kMaxDop], rows = 0;
+  xch_counts(x, dir, sr, rr);
+  for (int q = 0; q < x.P; ++q) rows += rr[q];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int n = 0;
+  timed(r, K_EXCH, s, 0, [&] {
+    n = xch_unpack(static_cast<const float*>(recv), dir == 0 ? r->x_tp : r->x_sp, x, dir, rows, s);
+    return 0;
+  });
+  g_launches += (unsigned long long)n;
+  return check_cuda("xch_unpack");
 }
 
 DDIT_API int ddit_request_profile(ddit_req* r, int enable) {

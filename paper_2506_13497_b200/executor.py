@@ -56,6 +56,31 @@ def latent_gather(dst: torch.Tensor, t_lo: int, t_hi: int, sources: list[tuple[t
     check(lib().ddit_latent_gather(dst.data_ptr(), t_lo, t_hi, P, lo, hi, n, C, HW, stream_ptr(stream)))
 
 
+def reshard(new_ranks: list[StepRequest], new_shards: list[torch.Tensor], old_ranks: list[StepRequest],
+            old_shards: list[torch.Tensor], streams=None) -> None:
+    """Promotion P -> P' in one C call (``ddit_reshard``): every new rank, on its own device
+    (and stream), gathers its frames from the old shards and takes the text state of old rank 0
+    (1.4 MB y-embedding + local cross-K/V recompute)."""
+    q, p = len(new_ranks), len(old_ranks)
+    nr = (vp * q)(*[r.handle.value for r in new_ranks])
+    nz = (vp * q)(*[z.data_ptr() for z in new_shards])
+    oz = (vp * p)(*[z.data_ptr() for z in old_shards])
+    lo = (ci * p)(*[r.shard.t_lo for r in old_ranks])
+    hi = (ci * p)(*[r.shard.t_hi for r in old_ranks])
+    st = (vp * q)(*[s.cuda_stream for s in streams]) if streams is not None else None
+    check(lib().ddit_reshard(nr, nz, q, oz, lo, hi, p, old_ranks[0].handle, st))
+
+
+def reshard_seconds(ranks: list[StepRequest]) -> list[float]:
+    """Device seconds of the last ``reshard`` into each rank (synchronises on it)."""
+    out = []
+    for r in ranks:
+        ms = ctypes.c_float()
+        check(lib().ddit_request_reshard_ms(r.handle, ctypes.byref(ms)))
+        out.append(ms.value / 1e3)
+    return out
+
+
 def exchange_bytes(sh: VideoShape, P: int, rank: int, C: int, B: int = 2) -> int:
     """Bytes rank ``rank`` of a DoP-P group pushes to its peers in one step: 28 spatial->temporal
     exchanges (its T-shard rows outside its own S-shard) + 28 temporal->spatial ones (its S-shard
@@ -90,7 +115,7 @@ class B200Executor:
                  shapes: dict[str, VideoShape] | None = None, num_steps: int = 30,
                  guidance: float = 7.0, seed_base: int = 0, vae_cfg=None, vae_weights=None,
                  keep_videos: bool = False, emulate_group: bool = False,
-                 nvlink_gbs: float = 770.0):
+                 nvlink_gbs: float = 770.0, latent_dir: str | None = None):
         self.cfg = cfg
         self.ndev = max(torch.cuda.device_count(), 1)
         self.models: dict[int, STDiTModel] = {}
@@ -117,7 +142,11 @@ class B200Executor:
         self.nvlink_gbs = nvlink_gbs
         self.pool: dict[tuple, list[_Live]] = {}  # (resolution, devices) -> idle groups
         self.pool_limit = 4
-        self.reshard_host_seconds: list[float] = []
+        self.reshard_host_seconds: list[float] = []  # promotion wall time, device wait included
+        self.reshard_enqueue_seconds: list[float] = []  # host work to enqueue the re-shard
+        # when set, every request's denoised latent (+ frames with keep_videos) is also written
+        # in the latent_io on-disk format as the DiT group hands it off
+        self.latent_dir = latent_dir
 
     # ---------------------------------------------------------------- helpers
     def device_of(self, gpu_id: int) -> int:
@@ -195,6 +224,25 @@ class B200Executor:
                                       device=torch.device("cuda", d)))
         return _Live(tuple(gpu_ids), ranks, shards, group, key=(request.resolution, tuple(devs)))
 
+    def preopen(self, resolutions, n_gpus: int) -> int:
+        """Open one pooled group per (resolution, buddy block) before serving: the single
+        GPUs, aligned pairs, quads and octet of an ``n_gpus`` node (15 groups for 8 GPUs) -- the
+        only shapes the greedy allocator hands out (reference allocator.py:221-234, :356-408).
+        A later start or promotion then re-binds an open group instead of allocating workspace,
+        building tables and GEMM / attention plans. Returns the number of groups opened."""
+        n = 0
+        for res in resolutions:
+            size = 1
+            while size <= n_gpus:
+                for start in range(0, n_gpus - size + 1, size):
+                    ids = tuple(range(start, start + size))
+                    probe = RequestState(1_000_000_000 + n, res, 0.0, self.num_steps)
+                    live = self._open_new(probe, ids)
+                    self.pool.setdefault(live.key, []).append(live)
+                    n += 1
+                size *= 2
+        return n
+
     # ---------------------------------------------------------------- StepExecutor protocol
     def dit_step(self, request: RequestState, gpu_ids: tuple[int, ...], step: int,
                  resharded_from: tuple[int, ...] | None) -> float:
@@ -208,24 +256,17 @@ class B200Executor:
             self.live[request.request_id] = live
         elif tuple(gpu_ids) != live.gpu_ids:  # promotion P -> P': re-shard at the boundary
             new = self._open(request, gpu_ids, text_from=live.ranks[0])
-            srcs = [(zs, r.shard.t_lo, r.shard.t_hi) for r, zs in zip(live.ranks, live.shards)]
-            spans = []
-            for r, zs in zip(new.ranks, new.shards):
-                with torch.cuda.device(zs.device):
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record()
-                    latent_gather(zs, r.shard.t_lo, r.shard.t_hi, srcs)
-                    r.copy_text_from(live.ranks[0])
-                    b.record()
-                    spans.append((a, b))
-            for d in {zs.device.index for zs in new.shards}:
-                torch.cuda.synchronize(d)
-            per = [a.elapsed_time(b) / 1e3 for a, b in spans]
+            # one C call: every new rank gathers its z frames (peer loads) and takes the text
+            # state (1.4 MB y-embedding + local cross-K/V recompute) on its own device
+            reshard(new.ranks, new.shards, live.ranks, live.shards)
+            t_enq = time.perf_counter()
+            per = reshard_seconds(new.ranks)
             one_device = len({zs.device.index for zs in new.shards}) == 1
             # ranks on P GPUs re-shard concurrently; virtual ranks on one device ran one by one
             dev_s = max(per) if (self.emulate_group or not one_device) else sum(per)
             self.reshard_seconds.append(dev_s)
             self.reshard_host_seconds.append(time.perf_counter() - t0)
+            self.reshard_enqueue_seconds.append(t_enq - t0)
             new.steps_done = live.steps_done
             new.history = live.history + [live.gpu_ids]
             self._close(live)
@@ -304,6 +345,17 @@ class B200Executor:
             self.videos[request.request_id] = (
                 parts[0] if len(parts) == 1
                 else torch.cat([v.to(torch.device("cuda", master)) for v in parts], dim=2))
+        if self.latent_dir is not None:
+            from pathlib import Path
+
+            from .latent_io import save_latent
+
+            Path(self.latent_dir).mkdir(parents=True, exist_ok=True)
+            save_latent(Path(self.latent_dir) / f"req{request.request_id}.ddlat",
+                        self.final_latents[request.request_id], request_id=request.request_id,
+                        resolution=request.resolution, steps=live.steps_done,
+                        frames=self.videos.get(request.request_id), dit_gpu_ids=list(dit_gpu_ids),
+                        vae_gpu_ids=list(vae_gpu_ids))
         decodes += [0.0] * (len(handoffs) - len(decodes))
         slowest = max(range(len(handoffs)), key=lambda i: handoffs[i] + decodes[i])
         self.vae_seconds.append((request.request_id, handoffs[slowest], decodes[slowest]))

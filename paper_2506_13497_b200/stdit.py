@@ -191,6 +191,11 @@ class StepRequest:
         when src lives on another GPU) -- the promotion-time state transfer."""
         check(lib().ddit_request_copy_text(self.handle, src.handle, stream_ptr(stream)))
 
+    def share_text_from(self, src: "StepRequest", stream=None) -> None:
+        """Promotion-time text state: copy src's 1.4 MB y-embedding (peer copy across GPUs) and
+        recompute the cross-attention K/V cache on this rank's GPU (bit-identical to copying it)."""
+        check(lib().ddit_request_share_text(self.handle, src.handle, stream_ptr(stream)))
+
     def exchange_buffers(self) -> tuple[int, int, int]:
         a, b, c = vp(), vp(), vp()
         check(lib().ddit_request_exchange_buffers(self.handle, ctypes.byref(a), ctypes.byref(b),
@@ -225,6 +230,20 @@ class StepRequest:
         self.step(z_dev, step, stream)
         z_host.copy_(z_dev, non_blocking=True)
         return z_host
+
+    # staged all-to-all (DDIT_OPT_EXTERNAL_XCH): the caller moves the rows between phases
+    def xch_counts(self, phase: int) -> tuple[list[int], list[int]]:
+        """Rows (of C fp32) this rank sends to / receives from every rank after ``phase``."""
+        P = self.desc.dop
+        snd, rcv = (ci * P)(), (ci * P)()
+        check(lib().ddit_request_xch_counts(self.handle, phase, snd, rcv))
+        return list(snd), list(rcv)
+
+    def xch_pack(self, phase: int, send: torch.Tensor, stream=None) -> None:
+        check(lib().ddit_request_xch_pack(self.handle, phase, send.data_ptr(), stream_ptr(stream)))
+
+    def xch_unpack(self, phase: int, recv: torch.Tensor, stream=None) -> None:
+        check(lib().ddit_request_xch_unpack(self.handle, phase, recv.data_ptr(), stream_ptr(stream)))
 
     def set_peers(self, x_sp: list[int], x_tp: list[int], flags: list[int] | None) -> None:
         n = len(x_sp)
@@ -299,6 +318,57 @@ class VirtualGroup:
             spans[i].append((a, ev()))
         s.synchronize()
         return [sum(a.elapsed_time(b) for a, b in sp) for sp in spans]
+
+
+DDIT_OPT_TC_ATTENTION = 1
+DDIT_OPT_EXTERNAL_XCH = 2
+
+
+class StagedVirtualGroup(VirtualGroup):
+    """DoP-P on one device with the staged exchange the NCCL arm uses: after every phase each
+    rank packs its outgoing rows per destination (``xch_pack``), the all-to-all is done by
+    concatenating send blocks into every rank's receive buffer on the device (what ncclAllToAllv
+    does between GPUs), and each rank unpacks (``xch_unpack``). Checks the pack/unpack layout
+    against DoP 1 without a second GPU."""
+
+    def __init__(self, model: STDiTModel, shape: VideoShape, y_cond, dop: int, **kw):
+        self.ranks = [StepRequest(model, shape, y_cond, dop=dop, rank=r, **kw) for r in range(dop)]
+        for r in self.ranks:
+            r.set_option(DDIT_OPT_EXTERNAL_XCH, 1)
+        self.depth = model.cfg.depth
+        self.C = model.cfg.hidden
+        self.counts = [[r.xch_counts(d) for d in (0, 1)] for r in self.ranks]
+        rows = max(max(sum(c[0]), sum(c[1])) for rc in self.counts for c in rc)
+        dev = model.device
+        self.send = [torch.empty((max(rows, 1), self.C), device=dev) for _ in self.ranks]
+        self.recv = [torch.empty((max(rows, 1), self.C), device=dev) for _ in self.ranks]
+
+    def all_to_all(self, phase: int, stream=None) -> None:
+        d = phase & 1
+        P = len(self.ranks)
+        for q in range(P):
+            off = 0
+            for r in range(P):
+                snd = self.counts[r][d][0]
+                lo = sum(snd[:q])
+                n = snd[q]
+                self.recv[q][off:off + n].copy_(self.send[r][lo:lo + n])
+                off += n
+
+    def step(self, z_parts: list[torch.Tensor], step: int, stream=None) -> list[torch.Tensor]:
+        for r, z in zip(self.ranks, z_parts):
+            r.begin(z, step, stream)
+        for k in range(2 * self.depth):
+            for r in self.ranks:
+                r.phase(k, stream)
+            for r, sb in zip(self.ranks, self.send):
+                r.xch_pack(k, sb, stream)
+            self.all_to_all(k, stream)
+            for r, rb in zip(self.ranks, self.recv):
+                r.xch_unpack(k, rb, stream)
+        for r, z in zip(self.ranks, z_parts):
+            r.end(z, step, stream)
+        return z_parts
 
 
 def launch_count() -> int:

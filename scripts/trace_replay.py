@@ -112,6 +112,9 @@ def main() -> None:
         t1 = time.time()
         rex = B200Executor(cfg, W, num_steps=a.steps, emulate_group=True, vae_cfg=OPENSORA_VAE,
                            vae_weights=vW)
+        tp = time.time()
+        ngroups = rex.preopen(LABELS, 8)  # the 15 buddy groups per resolution, opened up front
+        t_pre = time.time() - tp
         res = sched.Simulation(topo, table, dt, workload(r), sched.GreedyPolicy(dt), executor=rex).run()
         steps = len(rex.step_seconds)
         out["replayed"][f"{r:g}"] = {
@@ -120,6 +123,14 @@ def main() -> None:
             "reshard_ms_max": round(1e3 * max(rex.reshard_seconds), 3) if rex.reshard_seconds else None,
             "reshard_host_ms_max": (round(1e3 * max(rex.reshard_host_seconds), 3)
                                     if rex.reshard_host_seconds else None),
+            "reshard_host_ms_mean": (round(1e3 * sum(rex.reshard_host_seconds)
+                                           / len(rex.reshard_host_seconds), 3)
+                                     if rex.reshard_host_seconds else None),
+            "reshard_enqueue_ms_max": (round(1e3 * max(rex.reshard_enqueue_seconds), 3)
+                                       if rex.reshard_enqueue_seconds else None),
+            "reshard_ms_mean": (round(1e3 * sum(rex.reshard_seconds) / len(rex.reshard_seconds), 3)
+                                if rex.reshard_seconds else None),
+            "preopened_groups": ngroups, "preopen_seconds": round(t_pre, 2),
             "handoff_ms_max": round(1e3 * max(h for _, h, _ in rex.vae_seconds), 3),
             "wall_seconds": round(time.time() - t1, 1)}
         print("replayed", r, out["replayed"][f"{r:g}"], flush=True)

@@ -137,9 +137,10 @@ def test_vae_dop_splits_micro_batches(cuda, vae_dop):
     assert torch.equal(torch.cat(parts, dim=2), full)
 
 
-def test_engine_with_vae_dop2(cuda):
+def test_engine_with_vae_dop2(cuda, tmp_path):
     """Decoupled DiT(DoP 4) -> VAE(DoP 2) (BASELINE config 4): the policy keeps the two lowest
-    GPUs, each decodes its micro-batches; the video equals decoding the DoP-1 latent."""
+    GPUs, each decodes its micro-batches; the video equals decoding the DoP-1 latent. The hand-off
+    is also spilled in the on-disk latent format and reads back exactly."""
     from paper_2506_13497_b200 import sched, shapes, weights, vae_weights as vw
     from paper_2506_13497_b200.executor import B200Executor
     from paper_2506_13497_b200.vae import VAEDecoder
@@ -147,7 +148,8 @@ def test_engine_with_vae_dop2(cuda):
     cfg = dataclasses.replace(weights.TINY, depth=1)
     W = weights.init_weights(cfg, seed=3)
     VW = vw.init_vae_weights(vw.TINY_VAE)
-    ex = B200Executor(cfg, W, num_steps=2, vae_cfg=vw.TINY_VAE, vae_weights=VW, keep_videos=True)
+    ex = B200Executor(cfg, W, num_steps=2, vae_cfg=vw.TINY_VAE, vae_weights=VW, keep_videos=True,
+                      latent_dir=str(tmp_path))
     t = sched.load_profiles(_profile_doc())
     dt = sched.derive_dop_table(t, vae_dop=2)
     wl = [sched.ArrivalRecord(0, 0.0, "144p", 2)]  # 144p x 51 frames: 3 micro-batches
@@ -158,3 +160,49 @@ def test_engine_with_vae_dop2(cuda):
     ref = VAEDecoder(vw.TINY_VAE, VW, cuda).decode(ex.final_latents[0], sh.frames, sh.height, sh.width)
     torch.cuda.synchronize()
     assert torch.equal(ex.videos[0], ref)
+    from paper_2506_13497_b200.latent_io import load_latent
+
+    z, frames, hdr = load_latent(tmp_path / "req0.ddlat")
+    assert torch.equal(z, ex.final_latents[0].cpu()) and torch.equal(frames, ex.videos[0].cpu())
+    assert hdr["dit_gpu_ids"] == [0, 1, 2, 3] and hdr["vae_gpu_ids"] == [0, 1]
+
+
+def test_wall_clock_engine_runs_groups_concurrently(cuda):
+    """§8(f)1: the serving loop on wall-clock time -- steps, re-shards and the async DiT->VAE
+    hand-off enqueued on per-group streams, STEP_COMPLETE / VAE_COMPLETE taken from CUDA events.
+    Every request finishes, promotions happen, and each final latent equals the same steps at
+    DoP 1 bit for bit (concurrency and async hand-off are numerically invisible)."""
+    from paper_2506_13497_b200 import sched, shapes, weights
+    from paper_2506_13497_b200.serving import AsyncB200Executor, WallClockSimulation
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W = weights.init_weights(cfg, seed=3)
+    steps = 8
+    ex = AsyncB200Executor(cfg, W, num_steps=steps)
+    t = sched.load_profiles(_profile_doc())
+    dt = sched.derive_dop_table(t)
+    wl = [sched.ArrivalRecord(0, 0.0, "144p-16f", 2), sched.ArrivalRecord(1, 0.0, "144p", steps),
+          sched.ArrivalRecord(2, 0.001, "144p-16f", 3), sched.ArrivalRecord(3, 0.002, "144p", 5),
+          sched.ArrivalRecord(4, 0.05, "144p-16f", 4)]
+    sim = WallClockSimulation(sched.ClusterTopology(1, 4), t, dt, wl, sched.GreedyPolicy(dt), ex)
+    res = sim.run()
+    kinds = [r.kind for r in res.trace]
+    assert kinds.count("vae_complete") == len(wl)
+    times = [r.time for r in res.trace]
+    assert times == sorted(times)
+    m = sched.compute_metrics(res)
+    print(f"wall-clock engine: avg {m.avg_latency * 1e3:.2f} ms p99 {m.p99_latency * 1e3:.2f} ms, "
+          f"{len(sim.device_seconds)} device completions, promotions {kinds.count('promotion')}")
+    model = STDiTModel(cfg, W, cuda)
+    torch.cuda.synchronize()
+    for rec in wl:
+        sh = shapes.shape_of(rec.resolution)
+        z, y = weights.synthetic_inputs(cfg, sh.latent, seed_z=2 * rec.request_id, seed_y=2 * rec.request_id + 1)
+        req = StepRequest(model, sh, y.to(cuda), num_steps=steps)
+        zd = z.to(cuda).contiguous()
+        for i in range(rec.denoise_steps):
+            req.step(zd, i)
+        torch.cuda.synchronize()
+        assert torch.equal(ex.final_latents[rec.request_id], zd), rec.request_id
+    ex.close()

@@ -217,6 +217,12 @@ def test_rebound_and_broadcast_text_state_match_fresh_requests(cuda):
     other.step(z_b, 4)
     torch.cuda.synchronize()
     assert torch.equal(z_a, z_ref) and torch.equal(z_b, z_ref)
+    fourth = StepRequest(model, sh, y.to(cuda))
+    fourth.share_text_from(fresh)  # y-embedding copied, cross K/V recomputed on this rank
+    z_c = z.to(cuda).contiguous()
+    fourth.step(z_c, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(z_c, z_ref)
 
 
 @pytest.mark.parametrize("dop", [4, 8])
@@ -237,3 +243,55 @@ def test_virtual_dop_long_clip_matches_dop1(cuda, dop):
     grp.step(parts, 9)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, dim=2), z1)
+
+
+@pytest.mark.parametrize("label", ["144p", "240p", "144p-16f"])
+@pytest.mark.parametrize("dop", [2, 4, 8])
+def test_staged_exchange_matches_dop1(cuda, dop, label):
+    """The NCCL arm's staged exchange (pack per destination -> all-to-all -> unpack per source;
+    the collective emulated on one device) reproduces the DoP-1 step bit for bit: checks the
+    pack / unpack layouts for ragged T and S shards and for ranks that own no frames."""
+    from paper_2506_13497_b200 import weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StagedVirtualGroup, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=2)
+    W, sh, z, y = _setup(cfg, label)
+    model = STDiTModel(cfg, W, cuda)
+    yd = y.to(cuda)
+    z1 = z.to(cuda).contiguous()
+    StepRequest(model, sh, yd).step(z1, 5)
+    grp = StagedVirtualGroup(model, sh, yd, dop)
+    parts = grp.split(z.to(cuda))
+    grp.step(parts, 5)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, dim=2), z1)
+
+
+def test_exchange_barrier_times_out_instead_of_hanging(cuda):
+    """A DoP-2 rank whose peer never signals: the flag-barrier spin gives up after the bound,
+    records the silent rank in the request status and the stream drains (no GPU hang)."""
+    import time
+
+    from paper_2506_13497_b200 import _lib, weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = dataclasses.replace(weights.TINY, depth=1)
+    W, sh, z, y = _setup(cfg, "144p-16f")
+    model = STDiTModel(cfg, W, cuda)
+    r0 = StepRequest(model, sh, y.to(cuda), dop=2, rank=0)
+    xs, xt, fl = r0.exchange_buffers()
+    r0.set_peers([xs, xs], [xt, xt], [fl, fl + 64])  # rank 1's flag slot: never written
+    lib = _lib.lib()
+    lib.ddit_set_exchange_timeout_ms(200)
+    try:
+        zl = z[:, :, r0.shard.t_lo:r0.shard.t_hi].to(cuda).contiguous()
+        r0.begin(zl, 0)
+        r0.phase(0)  # spatial block: rows pushed + this rank's epoch published; rank 1 is silent
+        t0 = time.time()
+        _lib.check(lib.ddit_step_barrier(r0.handle, _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        assert time.time() - t0 < 10
+        with pytest.raises(_lib.DditError, match="rank"):
+            r0.status()
+    finally:
+        lib.ddit_set_exchange_timeout_ms(0)
