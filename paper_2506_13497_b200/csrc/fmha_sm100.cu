@@ -37,6 +37,21 @@
 
 namespace ddit {
 
+// DDIT_FMHA_TRACE (experiment builds only): SM-clock timeline of CTA 0 -- per softmax group and
+// tile: S ready, MUFU token taken, exps done, P buffer free, P stored; per unit: O ready, O
+// stored; per MMA warp and tile: QK issued, PV issued. Read back with ddit_fmha_trace().
+#ifdef DDIT_FMHA_TRACE
+__device__ unsigned long long g_fm_trace[2048];
+#define FM_TRACE(idx) \
+  do {                \
+    if (blockIdx.x == 0) g_fm_trace[(idx) & 2047] = clock64(); \
+  } while (0)
+#else
+#define FM_TRACE(idx) \
+  do {                \
+  } while (0)
+#endif
+
 namespace fm {
 constexpr int BQ = 128, BKV = 128, THREADS = 384, KST = 2, VST = 2;
 constexpr int QA = 16384, QB = 4096, QT = QA + QB;  // one Q tile: 64-col SW128 + 16-col SW32 boxes
@@ -350,6 +365,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
               umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), idq, 1);
               umma_commit(&s_full[g]);
               umma_commit(&k_empty[kc % KST]);
+              FM_TRACE(1024 + g * 256 + (sn & 63) * 2);
               if (j == nk - 1) umma_commit(&q_empty[qi]);
             }
             __syncwarp();
@@ -376,6 +392,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
               }
               umma_commit(&pv_done[g]);
               umma_commit(&v_empty[vc % VST]);
+              FM_TRACE(1024 + g * 256 + (pn & 63) * 2 + 1);
             }
             __syncwarp();
             ++pn;
@@ -429,6 +446,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       float m = -INFINITY;
       for (int j = 0; j < nk; ++j, ++n) {
         mbar_wait(&s_full[g], n & 1);
+        const bool trc = quarter == 0 && lane == 0;
+        if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 0);
         tc_fence_after();
         uint32_t s[128];
         tmem_ld32(s_tm, s);
@@ -470,6 +489,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         // so each runs at the full SFU rate while the other does its max / P stores / waits,
         // instead of both contending in phase
         if (has1) mbar_wait(&exp_tok[g], (tk & 1) ^ (g == 0 ? 1 : 0));
+        if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 1);
         // exps first (packed bf16 P kept in the consumed s[] registers: chunk c -> s[4c..4c+3]),
         // so the MUFU work overlaps the tensor core finishing PV_{j-1}
         const float neg_m = -m;
@@ -512,6 +532,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             }
           }
         }
+        if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 2);
         if (has1) {  // hand the MUFU turn to the other group
           __syncwarp();
           if (lane == 31) mbar_arrive_relaxed(&exp_tok[g ^ 1]);
@@ -520,6 +541,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         if (j > 0) {
           // PV of the previous tile done: P buffer free, O complete through tile j-1
           mbar_wait(&pv_done[g], (n - 1) & 1);
+          if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 3);
           if (__any_sync(0xffffffffu, resc)) {
             tc_fence_after();
 #pragma unroll 1
@@ -547,9 +569,11 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 31) mbar_arrive(&p_full[g]);  // release (P stores), from a lane without bulk copies
+        if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 4);
       }
       // ---- unit epilogue: O / l -> bf16 -> staging (the P buffer, 144 B rows) -> TMA store
       mbar_wait(&pv_done[g], (n - 1) & 1);
+      if (quarter == 0 && lane == 0) FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 5);
       tc_fence_after();
       uint32_t o[80];  // columns 0..71: O, column 72: the row sum l (ones column of V)
       tmem_ld32(o_tm, o);
@@ -574,6 +598,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       if (elected) {
         tma_store_4d(&tmO, pbuf, 0, p.o_slot + head, qt * BQ, seq);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 6);
       }
     }
     if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -705,6 +730,13 @@ int fmha_plan_launch(const FmhaPlan* fp, cudaStream_t s) {
 }
 
 }  // namespace ddit
+
+#ifdef DDIT_FMHA_TRACE
+extern "C" __attribute__((visibility("default"))) int ddit_fmha_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, ddit::g_fm_trace,
+                                   sizeof(unsigned long long) * (n < 2048 ? n : 2048));
+}
+#endif
 
 extern "C" DDIT_API int ddit_attention_tc(const ddit_attn* a, void* stream) {
   ddit::FmhaPlan fp;
