@@ -1,5 +1,11 @@
 """VAE decode on the B200 (tcgen05 implicit-GEMM convs + GroupNorm/attention kernels) vs the fp32
-CPU oracle (oracle/vae.py), reduced widths (TINY_VAE), micro-batched temporal decode."""
+CPU oracle (oracle/vae.py), reduced widths (TINY_VAE), micro-batched temporal decode.
+
+Tolerance: the decoder runs ~40 conv / GroupNorm / attention layers on bf16 activations (as the
+deployed OpenSora VAE does), so its distance to the fp32 oracle is set by bf16 rounding compounding
+over depth, not by the kernels. The bar is therefore relative to the SAME oracle run in bf16
+(torch CPU autocast: bf16 convs / matmuls, fp32 norms): ours must be within 1.1x of that
+stock-bf16 error (measured: ours 1.4-1.6e-2, stock bf16 1.6-1.8e-2), and never above 3e-2."""
 import pytest
 import torch
 
@@ -8,6 +14,12 @@ pytestmark = pytest.mark.gpu
 
 def rel_l2(a, b):
     return (torch.linalg.vector_norm(a.float() - b.float()) / torch.linalg.vector_norm(b.float())).item()
+
+
+def _stock_bf16(ovae, W, cfg, z, frames, H, Wd):
+    """The oracle decode under torch CPU bf16 autocast: what a stock bf16 implementation gets."""
+    with torch.autocast("cpu", dtype=torch.bfloat16):
+        return ovae.vae_decode(W, cfg, z, frames, H, Wd).float()
 
 
 @pytest.mark.parametrize("T,h,w,frames", [(4, 6, 10, 16), (15, 4, 6, 51), (2, 5, 7, 5)])
@@ -27,8 +39,9 @@ def test_vae_decode_matches_oracle(cuda, T, h, w, frames):
     torch.cuda.synchronize()
     assert out.shape == ref.shape
     err = rel_l2(out.cpu(), ref)
-    print(f"vae T={T} {h}x{w} frames={frames}: relL2 {err:.2e}")
-    assert err <= 2e-2
+    err_bf16 = rel_l2(_stock_bf16(ovae, W, cfg, z, frames, H, Wd), ref)
+    print(f"vae T={T} {h}x{w} frames={frames}: relL2 {err:.2e} (stock bf16 oracle {err_bf16:.2e})")
+    assert err <= 1.1 * err_bf16 and err <= 3e-2
 
 
 def test_full_width_vae_decode_matches_oracle(cuda):
@@ -45,8 +58,9 @@ def test_full_width_vae_decode_matches_oracle(cuda):
     out = VAEDecoder(cfg, W, cuda).decode(z.to(cuda), 16, 144, 256)
     torch.cuda.synchronize()
     err = rel_l2(out.cpu(), ref)
-    print(f"full-width vae 144p x16: relL2 {err:.2e}")
-    assert err <= 3e-2
+    err_bf16 = rel_l2(_stock_bf16(ovae, W, cfg, z, 16, 144, 256), ref)
+    print(f"full-width vae 144p x16: relL2 {err:.2e} (stock bf16 oracle {err_bf16:.2e})")
+    assert err <= 1.1 * err_bf16 and err <= 3e-2
 
 
 def test_graph_replay_equals_eager(cuda):
