@@ -46,6 +46,10 @@ DDIT_API int ddit_set_gemm_2cta(int on);
  * memory over NVLink) and the kernel's last CTA publishes the exchange flag; 0 = the separate
  * exchange kernel. Default 1 (env DDIT_FUSED_XCH=0); applies to peers registered afterwards. */
 DDIT_API int ddit_set_fused_exchange(int on);
+/* Gated-residual GEMMs without a bf16 copy or fused exchange: 1 (default) = the update leaves
+ * through a TMA reduce-add into the fp32 residual (no residual loads), 0 = TMA load / update /
+ * store. Both give bit-identical results. Env DDIT_RESID_RED=0; applies to plans built afterwards. */
+DDIT_API int ddit_set_resid_reduce(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */
@@ -245,8 +249,9 @@ DDIT_API int ddit_set_exchange_timeout_ms(int ms);
 /* Device timestep (after the RFLOW transform) and dt of a step, for logging / tests. */
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
 
-/* Request options: DDIT_OPT_TC_ATTENTION (default 1) selects the tcgen05 FMHA for spatial /
- * cross attention; 0 falls back to the mma.sync flash kernel (kept as the baseline). */
+/* Request options: DDIT_OPT_TC_ATTENTION is retired -- spatial / cross attention always run the
+ * tcgen05 FMHA (value 1 is accepted, 0 returns DDIT_E_INVALID; the mma.sync flash kernel is
+ * reachable only through ddit_attention, as a test cross-check). */
 #define DDIT_OPT_TC_ATTENTION 1
 /* DDIT_OPT_EXTERNAL_XCH (default 0): the step does not exchange rows itself (no peers, no fused
  * fc2 stores, no flag barrier); after every ddit_step_phase the caller moves them with

@@ -128,6 +128,7 @@ _SIGNATURES = {
     "ddit_set_gemm_2cta": [ci],
     "ddit_set_pdl": [ci],
     "ddit_set_fused_exchange": [ci],
+    "ddit_set_resid_reduce": [ci],
     "ddit_set_exchange_timeout_ms": [ci],
     "ddit_enable_peer_access": [ci, ci],
     "ddit_attention": [ctypes.POINTER(Attn), vp],

@@ -76,6 +76,10 @@ DDIT_API int ddit_set_pdl(int on) {
   set_pdl(on);
   return DDIT_OK;
 }
+DDIT_API int ddit_set_resid_reduce(int on) {
+  set_resid_red(on);
+  return DDIT_OK;
+}
 DDIT_API int ddit_set_gemm_2cta(int on) {
   set_two_cta(on);
   return DDIT_OK;

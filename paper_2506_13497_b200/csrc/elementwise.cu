@@ -74,7 +74,67 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-static int g_ln_variant = -1;  // tuning hook (env DDIT_LN): 0 generic, 1 = 32 lanes x 9, 2 = 16 x 18
+// C = 1152 streaming variant: a persistent grid of warps, each walking rows r, r + nwarps, ...
+// with the NEXT row's 9 float4 per lane loaded before the current row's reductions and stores,
+// so every warp keeps a row of loads in flight across its whole life (no block-launch tails).
+__global__ void __launch_bounds__(256)
+    ln_modulate_stream_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int M,
+                              const float* __restrict__ shift, const float* __restrict__ scale,
+                              int mod_stride, int rows_per_b, float eps) {
+  constexpr int C = 1152, NV = 9;
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= M) return;
+  float4 v[NV];
+  {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = __ldcs(xr + lane + 32 * i);
+  }
+  for (;;) {
+    const int next = row + nw;
+    float4 nx[NV];
+    if (next < M) {
+      const float4* xr = reinterpret_cast<const float4*>(x + (size_t)next * C);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) nx[i] = __ldcs(xr + lane + 32 * i);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = group_sum<32>(s) * (1.f / C);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
+    const float rstd = rsqrtf(group_sum<32>(q) * (1.f / C) + eps);
+    const int bidx = row / rows_per_b;
+    const float4* sh = reinterpret_cast<const float4*>(shift + (size_t)bidx * mod_stride);
+    const float4* sc = reinterpret_cast<const float4*>(scale + (size_t)bidx * mod_stride);
+    uint2* o = reinterpret_cast<uint2*>(out + (size_t)row * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + 32 * i;
+      const float4 a = __ldg(sh + c), k = __ldg(sc + c);
+      const float y0 = (v[i].x - mean) * rstd * (1.f + k.x) + a.x;
+      const float y1 = (v[i].y - mean) * rstd * (1.f + k.y) + a.y;
+      const float y2 = (v[i].z - mean) * rstd * (1.f + k.z) + a.z;
+      const float y3 = (v[i].w - mean) * rstd * (1.f + k.w) + a.w;
+      o[c] = make_uint2(pack_bf16(y0, y1), pack_bf16(y2, y3));
+    }
+    if (next >= M) break;
+    row = next;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = nx[i];
+  }
+}
+
+static int g_ln_variant = -1;  // tuning hook (env DDIT_LN): 0 generic, 1 = 32 lanes x 9, 2 = 16 x 18,
+                               // 3 = persistent streaming warps
 
 int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
                 const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s) {
@@ -84,7 +144,21 @@ int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* s
     g_ln_variant = e ? atoi(e) : 1;
   }
   const int rpb = rows_per_b > 0 ? rows_per_b : M;
-  if (C == 1152 && g_ln_variant == 1) {
+  if (C == 1152 && g_ln_variant == 3) {
+    static int grid_cap = 0;
+    if (!grid_cap) {
+      int dev = 0, sms = 148, bps = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ln_modulate_stream_kernel, 256, 0);
+      const char* e = getenv("DDIT_LN_BPS");
+      if (e && atoi(e) > 0 && atoi(e) < bps) bps = atoi(e);
+      grid_cap = sms * (bps > 0 ? bps : 1);
+    }
+    const int need = (M + 7) / 8;
+    launch_pdl(ln_modulate_stream_kernel, dim3(need < grid_cap ? need : grid_cap), dim3(256), 0, s,
+               x, out, M, shift, scale, mod_stride, rpb, eps);
+  } else if (C == 1152 && g_ln_variant == 1) {
     launch_pdl(ln_modulate_kernel<9, 32, true>, dim3((M + 3) / 4), dim3(128), 0, s, x, out, M, C,
                shift, scale, mod_stride, rpb, eps);
   } else if (C == 1152 && g_ln_variant == 2) {

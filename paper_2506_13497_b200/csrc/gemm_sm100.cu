@@ -28,10 +28,15 @@ static constexpr int kThreads = 256;
 static constexpr int kTmemCols = 512;
 static constexpr int kAccStride = 256;  // TMEM column offset of accumulator buffer 1
 
-__host__ __device__ constexpr bool is_resid(int epi) { return epi == EPI_RESID || epi == EPI_RESID_COPY; }
+__host__ __device__ constexpr bool is_resid(int epi) {
+  return epi == EPI_RESID || epi == EPI_RESID_COPY || epi == EPI_RESID_RED;
+}
 
 #ifndef DDIT_RSLOTS
 #define DDIT_RSLOTS 2
+#endif
+#ifndef DDIT_RED_BUFS
+#define DDIT_RED_BUFS 2
 #endif
 // DDIT_EPI_TRACE (experiment builds only): SM-clock timestamps of CTA 0's MMA issuer and first
 // epilogue warp per tile / sub-tile, read back with ddit_debug_trace()
@@ -55,7 +60,8 @@ struct EpiCfg {
   static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
   // gated residual: each epilogue warp runs its own ring of RSLOTS fp32 32x32 sub-tiles (loads run
   // RSLOTS-2 sub-tiles ahead) + three bf16 copy buffers (SW64): WARP_BYTES per warp
-  static constexpr int RSLOTS = is_resid(EPI) ? DDIT_RSLOTS : 0;
+  static constexpr bool RED = EPI == EPI_RESID_RED;
+  static constexpr int RSLOTS = is_resid(EPI) ? (RED ? DDIT_RED_BUFS : DDIT_RSLOTS) : 0;
   // R >= 3: stores of sub-tile s-1 may still read while s runs (3 bf16 buffers, loads R-2 ahead);
   // R == 2: they must finish first (2 bf16 buffers, loads 1 ahead)
   static constexpr int RAHEAD = RSLOTS >= 3 ? RSLOTS - 2 : 1;
@@ -66,6 +72,8 @@ struct EpiCfg {
   // EPI_RESID with BN % 64 == 0 never has a bf16 copy (the plan turns out2 into EPI_RESID_COPY),
   // so its copy buffers are not allocated: the smem goes back to the mainloop (fc2: 6 stages)
   static constexpr bool HAS_OB = EPI == EPI_RESID_COPY || (EPI == EPI_RESID && BN % 64 != 0);
+  // EPI_RESID_RED: RSLOTS staging buffers per warp, each a 32 x 32 fp32 sub-tile on its way out
+  // through a TMA reduce-add (no loads, no bf16 copy)
   static constexpr int WARP_BYTES = RSLOTS * 4096 + (HAS_OB ? NOB * OB : 0);
   // gated residual: the bias row and the B gate rows (all N columns) staged once per CTA, so the
   // per-sub-tile column vectors are shared-memory broadcasts instead of cold L2 reads (consecutive
@@ -438,10 +446,12 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 b = bv[j], g = gv[j], x = xv[j];
-      nv[4 * j + 0] = x.x + g.x * (__uint_as_float(r[4 * j + 0]) + b.x);
-      nv[4 * j + 1] = x.y + g.y * (__uint_as_float(r[4 * j + 1]) + b.y);
-      nv[4 * j + 2] = x.z + g.z * (__uint_as_float(r[4 * j + 2]) + b.z);
-      nv[4 * j + 3] = x.w + g.w * (__uint_as_float(r[4 * j + 3]) + b.w);
+      // x + (g * (acc + b)) rounded step by step (no FMA contraction): the reduce-add epilogue
+      // (EPI_RESID_RED) computes exactly this, so DoP-P ranks that exchange stay bit-exact
+      nv[4 * j + 0] = __fadd_rn(x.x, __fmul_rn(g.x, __fadd_rn(__uint_as_float(r[4 * j + 0]), b.x)));
+      nv[4 * j + 1] = __fadd_rn(x.y, __fmul_rn(g.y, __fadd_rn(__uint_as_float(r[4 * j + 1]), b.y)));
+      nv[4 * j + 2] = __fadd_rn(x.z, __fmul_rn(g.z, __fadd_rn(__uint_as_float(r[4 * j + 2]), b.z)));
+      nv[4 * j + 3] = __fadd_rn(x.w, __fmul_rn(g.w, __fadd_rn(__uint_as_float(r[4 * j + 3]), b.w)));
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -489,6 +499,81 @@ DDIT_DEV void epi_resid_tile(const EpiParams& ep, const CUtensorMap* tmR, const 
       }
     }
     if (ew == 0 && lane == 0) EPI_TRACE(640 + 16 * (cnt / NS) + sub);
+    ++cnt;
+  }
+}
+
+DDIT_DEV void tma_reduce_add_2d(const void* tmap, const void* smem_src, int c0, int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// x[r, c] += gate[b(r), c] * (acc + bias[c]) without reading x: every warp stages y = gate *
+// (acc + bias) for its 32 rows x 32 columns in a ring of RSLOTS swizzled fp32 buffers and sends
+// it to x with a TMA reduce-add (the L2 computes x + y, round-to-nearest -- the same two
+// roundings as the load / update / store path, which keeps DoP-P bit-exact). The only wait is for
+// a buffer's previous reduce to finish reading shared memory, RSLOTS - 1 sub-tiles later.
+template <int BN>
+DDIT_DEV void epi_red_tile(const EpiParams& ep, const CUtensorMap* tmR, uint8_t* sE,
+                           uint32_t taddr, int ew, int lane, int m0, int n0, const EpiCtx& cx,
+                           int& cnt, uint32_t tempty_cl, const float* sCol) {
+  constexpr int NS = BN / 32;
+  using Cfg = EpiCfg<BN, EPI_RESID_RED>;
+  constexpr int R = Cfg::RSLOTS;
+  uint8_t* wbase = sE + ew * Cfg::WARP_BYTES;
+  const int row = m0 + ew * 32 + lane;
+  const int grow = row < cx.M ? row : cx.M - 1;
+  const float* gate_row = ep.gate ? ep.gate + (size_t)(grow / ep.rows_per_b) * ep.gate_stride : nullptr;
+  const float* s_gate = sCol && ep.gate ? sCol + (size_t)(1 + grow / ep.rows_per_b) * cx.N : nullptr;
+#pragma unroll 1
+  for (int sub = 0; sub < NS; ++sub) {
+    uint8_t* rb = wbase + (cnt % R) * 4096;
+    const int col0 = n0 + sub * 32;
+    float4 bv[8], gv[8];
+    if (sCol) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bv[j] = reinterpret_cast<const float4*>(sCol + col0)[j];
+        gv[j] = s_gate ? reinterpret_cast<const float4*>(s_gate + col0)[j] : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bv[j] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + col0) + j)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[j] = gate_row ? __ldg(reinterpret_cast<const float4*>(gate_row + col0) + j)
+                         : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+    }
+    uint32_t r[32];
+    tmem_ld_x32(taddr + sub * 32, r);
+    if (lane == 0) bulk_wait_read<R - 1>();  // the reduce that last used this buffer has read it
+    tmem_ld_wait();
+    if (sub == NS - 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 31) mbar_arrive_cl_relaxed(tempty_cl);
+    }
+    __syncwarp();
+    const uint32_t rbase = smem_u32(rb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 b = bv[j], g = gv[j];
+      st_shared_v4(rbase + sw128(lane, j),
+                   __float_as_uint(__fmul_rn(g.x, __fadd_rn(__uint_as_float(r[4 * j + 0]), b.x))),
+                   __float_as_uint(__fmul_rn(g.y, __fadd_rn(__uint_as_float(r[4 * j + 1]), b.y))),
+                   __float_as_uint(__fmul_rn(g.z, __fadd_rn(__uint_as_float(r[4 * j + 2]), b.z))),
+                   __float_as_uint(__fmul_rn(g.w, __fadd_rn(__uint_as_float(r[4 * j + 3]), b.w))));
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_reduce_add_2d(tmR, rb, col0, m0 + ew * 32);
+      bulk_commit();
+    }
     ++cnt;
   }
 }
@@ -709,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         resid_prefetch_l2<BN>(rs, 0, &tmO);
         resid_prefetch_l2<BN>(rs, 1, &tmO);
       }
-      if (lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
+      if (EPI != EPI_RESID_RED && lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
         for (int j = 0; j < EpiCfg<BN, EPI>::RAHEAD; ++j)
           resid_issue<R>(rs, BN / 32, j, ew * 32, &tmR, sE + ew * EpiCfg<BN, EPI>::WARP_BYTES, rbar + ew * R);
     }
@@ -729,6 +814,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+      } else if constexpr (EPI == EPI_RESID_RED) {
+        epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
       } else if constexpr (is_resid(EPI)) {
         epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
@@ -943,7 +1030,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         resid_prefetch_l2<BN>(rs, 0, &tmO);
         resid_prefetch_l2<BN>(rs, 1, &tmO);
       }
-      if (lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
+      if (EPI != EPI_RESID_RED && lane == 0)  // the first R-2 residual sub-tiles of this warp's slab
         for (int j = 0; j < EpiCfg<BN, EPI>::RAHEAD; ++j)
           resid_issue<R>(rs, BN / 32, j, ew * 32, &tmR, sE + ew * EpiCfg<BN, EPI>::WARP_BYTES, rbar + ew * R);
     }
@@ -963,6 +1050,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
         epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+      } else if constexpr (EPI == EPI_RESID_RED) {
+        epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
       } else if constexpr (is_resid(EPI)) {
         epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
       } else {
@@ -1131,8 +1220,12 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
       break;
     case EPI_RESID:
     case EPI_RESID_COPY:
-      // with a bf16 copy and BN % 64 == 0, the copy leaves in 64-column boxes (EPI_RESID_COPY)
+    case EPI_RESID_RED:
+      // with a bf16 copy and BN % 64 == 0, the copy leaves in 64-column boxes (EPI_RESID_COPY);
+      // without copy or exchange the update is a TMA reduce-add (EPI_RESID_RED)
       if (ep.out2 && bn % 64 == 0) epi = EPI_RESID_COPY;
+      if (!ep.out2 && !ep.xch && resid_red_enabled()) epi = EPI_RESID_RED;
+      if (epi == EPI_RESID_RED && (ep.out2 || ep.xch)) epi = EPI_RESID;
       if (epi == EPI_RESID_COPY && (!ep.out2 || bn % 64)) {
         snprintf(g_err, sizeof g_err, "EPI_RESID_COPY needs out2 and BN %% 64 == 0");
         return -2;
@@ -1170,6 +1263,16 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
   }
   return 0;
 }
+
+static int g_resid_red = -1;
+bool resid_red_enabled() {
+  if (g_resid_red < 0) {
+    const char* e = getenv("DDIT_RESID_RED");
+    g_resid_red = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_resid_red != 0;
+}
+void set_resid_red(int on) { g_resid_red = on ? 1 : 0; }
 
 static int g_pdl = -1;
 bool pdl_enabled() {
@@ -1259,6 +1362,14 @@ int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
         case 128: return launch_t<128, EPI_RESID>(p, s);
         case 192: return launch_t<192, EPI_RESID>(p, s);
         case 256: return launch_t<256, EPI_RESID>(p, s);
+      }
+      break;
+    case EPI_RESID_RED:
+      switch (p->bn) {
+        case 96: return launch_t<96, EPI_RESID_RED>(p, s);
+        case 128: return launch_t<128, EPI_RESID_RED>(p, s);
+        case 192: return launch_t<192, EPI_RESID_RED>(p, s);
+        case 256: return launch_t<256, EPI_RESID_RED>(p, s);
       }
       break;
     case EPI_RESID_COPY:

@@ -16,6 +16,8 @@ enum EpiKind : int {
   EPI_QKV = 3,        // out_bf16 = rope(rmsnorm_head(acc + bias)) on the q/k sections; v: acc + bias
   EPI_F32 = 4,        // out_f32 = acc + bias
   EPI_RESID_COPY = 5, // internal: EPI_RESID with the bf16 copy, stored in 64-column (128 B) boxes
+  EPI_RESID_RED = 6,  // internal: EPI_RESID without copy / exchange: gate * (acc + bias) leaves
+                      // through a TMA reduce-add into resid (the L2 does x + y; nothing is loaded)
 };
 
 struct EpiParams {
@@ -75,6 +77,8 @@ void gemm_pick_tile(int M, int N, int epi, int* bn, int* two_cta);
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
 int num_sms();
 bool two_cta_enabled();
+bool resid_red_enabled();
+void set_resid_red(int on);
 void set_pdl(int on);
 void set_two_cta(int on);
 const char* gemm_last_error();

@@ -157,7 +157,6 @@ struct ddit_req {
   PeerFlags peer_flags{};
   bool peers_set = false;
   bool flags_set = false;
-  bool use_tc_attention = true;  // tcgen05 FMHA for spatial / cross attention
   bool fused_xch = false;        // the fc2 GEMM of every block performs the DSP exchange
   bool external_xch = false;     // the caller moves the rows (staged pack -> ncclAllToAll -> unpack)
   // profiling: event pairs around every launch, tagged by kernel class
@@ -453,15 +452,22 @@ int build_attn_plans(ddit_req* r) {
   return DDIT_OK;
 }
 
+// Spatial and cross attention run the tcgen05 FMHA plan built at request open; there is no
+// other kernel for them on the step path (a layout the plan cannot take fails the step).
+// Temporal self-attention (T <= 32 keys per sequence) has its own kernel.
 int run_attn(ddit_req* r, int k, bool cross, cudaStream_t s) {
-  const std::vector<uint8_t>& ok = cross ? r->fm_cross_ok : r->fm_self_ok;
-  if (r->use_tc_attention && ok[k]) {
-    const FmhaPlan& fp = cross ? r->fm_cross[k] : r->fm_self[k];
-    return timed(r, K_ATTN, s, 1, [&] { return fmha_plan_launch(&fp, s); });
+  if (!cross && (k & 1)) {
+    ddit_attn a = self_attn_args(r, k);
+    return attn_temporal(r, &a, s);
   }
-  ddit_attn a = cross ? cross_attn_args(r, k) : self_attn_args(r, k);
-  if (!cross && (k & 1)) return attn_temporal(r, &a, s);
-  return attn(r, &a, s);
+  const std::vector<uint8_t>& ok = cross ? r->fm_cross_ok : r->fm_self_ok;
+  if (!ok[k]) {
+    set_error("block %d: %s attention layout not supported by the tcgen05 FMHA", k,
+              cross ? "cross" : "spatial");
+    return DDIT_E_CONFIG;
+  }
+  const FmhaPlan& fp = cross ? r->fm_cross[k] : r->fm_self[k];
+  return timed(r, K_ATTN, s, 1, [&] { return fmha_plan_launch(&fp, s); });
 }
 
 int run_block(ddit_req* r, int k, cudaStream_t s) {
@@ -969,9 +975,10 @@ DDIT_API int ddit_set_fused_exchange(int on) {
 
 DDIT_API int ddit_request_set_option(ddit_req* r, int option, int value) {
   switch (option) {
-    case DDIT_OPT_TC_ATTENTION:
-      r->use_tc_attention = value != 0;
-      return DDIT_OK;
+    case DDIT_OPT_TC_ATTENTION:  // retired: the step has one attention path (tcgen05 FMHA)
+      if (value != 0) return DDIT_OK;
+      set_error("DDIT_OPT_TC_ATTENTION=0 is no longer supported: the step always runs the tcgen05 FMHA");
+      return DDIT_E_INVALID;
     case DDIT_OPT_EXTERNAL_XCH:
       r->external_xch = value != 0;
       return DDIT_OK;

@@ -77,6 +77,35 @@ def test_gemm_resid_gate(cuda, bn, N, K):
     assert rel_l2(x1, x0 + a.float() @ w.float().T + bias) < 1e-5
 
 
+@pytest.mark.parametrize("bn,two", [(192, 1), (128, 0), (96, 1), (256, 0)])
+def test_gemm_resid_reduce_matches_load_update_store(cuda, bn, two):
+    """The reduce-add residual epilogue (TMA reduce into x, nothing loaded) and the TMA load /
+    update / store epilogue give bit-identical x (both round acc + b, g * (.), x + (.) in turn),
+    which is what keeps DoP-P (whose fc2 exchanges rows) bit-exact with DoP 1."""
+    from paper_2506_13497_b200 import kernels, _lib
+
+    L = _lib.lib()
+    M, N, K = 2 * 1013, 1152, 1152
+    a, w, bias = _inputs(M, N, K, cuda, seed=5)
+    x0 = torch.randn(M, N, device=cuda)
+    gate = torch.randn(2, N, device=cuda)
+    outs = []
+    try:
+        L.ddit_set_gemm_2cta(two)
+        for red in (0, 1):
+            L.ddit_set_resid_reduce(red)
+            x = x0.clone()
+            kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=M // 2, bn=bn)
+            outs.append(x)
+    finally:
+        L.ddit_set_resid_reduce(1)
+        L.ddit_set_gemm_2cta(1)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    b = torch.arange(M, device=cuda) // (M // 2)
+    assert rel_l2(outs[1], x0 + gate[b] * (a.float() @ w.float().T + bias)) < 1e-5
+
+
 @pytest.mark.parametrize("rope", [False, True])
 def test_gemm_qkv_epilogue(cuda, rope):
     from paper_2506_13497_b200 import kernels, _lib
