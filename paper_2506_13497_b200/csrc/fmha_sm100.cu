@@ -289,11 +289,12 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
     if (warp == 0 && lane == 0) {  // ------------------------------------------ TMA producer
-      int kc = 0, vc = 0, qc[2] = {0, 0};
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int kc = 0, vc = 0, qc[2] = {0, 0}, ul = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
         int pr, head, seq;
         bool has1;
         decode(u, pr, head, seq, has1);
+        FM_TRACE(1792 + (ul & 63) * 4 + 0);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if (g == 1 && !has1) break;
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           tma_load_4d(qbuf + QA, &tmQb, &q_full[qi], 64, p.q_slot + head, (2 * pr + g) * BQ, seq);
           ++qc[g];
         }
+        FM_TRACE(1792 + (ul & 63) * 4 + 1);
         for (int j = 0; j < nk; ++j, ++kc, ++vc) {
           const int ks = kc % KST, vs = vc % VST;
           mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
@@ -312,11 +314,13 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           mbar_arrive_expect_tx(&k_full[ks], KA + KB);
           tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + head, j * BKV, seq);
           tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + head, j * BKV, seq);
+          if (j == 0) FM_TRACE(1792 + (ul & 63) * 4 + 2);
           mbar_wait(&v_empty[vs], ((vc / VST) & 1) ^ 1);
           uint8_t* vb = sm + OFF_V + vs * (VA + VB);
           mbar_arrive_expect_tx(&v_full[vs], VA + VB);
           tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + head, j * BKV, seq);
           tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
+          if (j == nk - 1) FM_TRACE(1792 + (ul & 63) * 4 + 3);
         }
       }
       pdl_trigger();
@@ -347,11 +351,15 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         }
         const int qi = g * 2 + (qc & 1);
         const uint32_t qa = smem_u32(sm + OFF_Q + qi * QT);
+        if (lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 0);
         mbar_wait(&q_full[qi], (qc >> 1) & 1);
+        if (lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 1);
         for (int j = 0; j <= nk; ++j) {
           if (j < nk) {  // S = Q K_j^T once the group holds its previous S in registers
             mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
+            if (j == 0 && lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 2);
             if (sn > 0) mbar_wait(&s_free[g], (sn - 1) & 1);
+            if (j == 0 && lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 3);
             tc_fence_after();
             if (elect_one()) {
               const uint32_t ka = smem_u32(sm + OFF_K + (kc % KST) * (KA + KB)), kb = ka + KA;
@@ -514,22 +522,28 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
-        } else {  // chunks past `valid` only get zero P (the tensor core still reads them)
+        } else {
+          // ragged last tile: PV reads only the round16(valid) keys QK wrote, so the loop leaves
+          // (a real branch, not predication -- a predicated tail costs a whole tile of MUFU issue)
+          // after the chunks holding them; keys in [valid, round16(valid)) get P = 0
+          const int kv16 = (valid + 15) & ~15;
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            if (c * 8 < valid) {
-              float pv[8];
+            if (c * 8 >= kv16) break;
+            float pv[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int key = c * 8 + e;
-                pv[e] = key < valid ? fast_exp2(fmaf(__uint_as_float(s[key]), p.scale_log2, neg_m)) : 0.f;
-              }
-#pragma unroll
-              for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) s[4 * c + e] = 0u;
+            for (int e = 0; e < 8; e += 2) {
+              float x0, x1;
+              ffma2(x0, x1, __uint_as_float(s[c * 8 + e]), __uint_as_float(s[c * 8 + e + 1]),
+                    p.scale_log2, neg_m);
+              pv[e] = fast_exp2(x0);
+              pv[e + 1] = fast_exp2(x1);
             }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (c * 8 + e >= valid) pv[e] = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[4 * c + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
           }
         }
         if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 2);
@@ -585,6 +599,10 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       __syncwarp();
       if (lane == 31) mbar_arrive_relaxed(&o_free[g]);
       const float inv = l > 0.f ? 1.f / l : 0.f;
+      // the O staging overwrites this group's P buffer: the last PV has read it (pv_done above);
+      // the named barrier also orders every warp's P stores before any O store for the
+      // sanitizer, which does not follow the tcgen05.commit -> mbarrier chain
+      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       const uint32_t obase = smem_u32(pbuf) + row * 144;
 #pragma unroll
       for (int c = 0; c < 9; ++c)

@@ -944,6 +944,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  __syncthreads();  // (a CTA barrier is implied; explicit for compute-sanitizer racecheck)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();

@@ -63,3 +63,17 @@ for grp in (0, 1):
         if row[0] < 0 and mm[0] < 0:
             continue
         print(f"  {n:3d}: " + " ".join(f"{x:7d}" for x in row) + "  " + " ".join(f"{x:7d}" for x in mm))
+
+print("MMA warps per unit: q_wait_start  q_full  k_full(t0)  s_free(t0)")
+for grp in (0, 1):
+    for u in range(32):
+        row = [rel(v[1536 + grp * 128 + u * 4 + k]) for k in range(4)]
+        if row[0] < 0:
+            continue
+        print(f"  g{grp} unit {u:2d}: " + " ".join(f"{x:7d}" for x in row))
+print("producer per unit: start  Q_issued  K(t0)_issued  V(last)_issued")
+for u in range(64):
+    row = [rel(v[1792 + u * 4 + k]) for k in range(4)]
+    if row[0] < 0:
+        continue
+    print(f"  unit {u:2d}: " + " ".join(f"{x:7d}" for x in row))
