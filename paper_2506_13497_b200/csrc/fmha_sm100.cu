@@ -289,12 +289,15 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
     if (warp == 0 && lane == 0) {  // ------------------------------------------ TMA producer
-      int kc = 0, vc = 0, qc[2] = {0, 0}, ul = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
+      // Loads go out in the order the MMA warps consume them -- K_j before V_{j-1} (QK_j is issued
+      // before PV_{j-1}), and the next unit's Q and K_0 before this unit's last V -- so a load
+      // never queues behind a V stage that frees only after a later softmax phase: the next
+      // unit's first QK can issue right after this unit's last PV.
+      int kc = 0, vc = 0, qc[2] = {0, 0};
+      auto load_q = [&](int u) {
         int pr, head, seq;
         bool has1;
         decode(u, pr, head, seq, has1);
-        FM_TRACE(1792 + (ul & 63) * 4 + 0);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if (g == 1 && !has1) break;
@@ -306,22 +309,47 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           tma_load_4d(qbuf + QA, &tmQb, &q_full[qi], 64, p.q_slot + head, (2 * pr + g) * BQ, seq);
           ++qc[g];
         }
-        FM_TRACE(1792 + (ul & 63) * 4 + 1);
-        for (int j = 0; j < nk; ++j, ++kc, ++vc) {
-          const int ks = kc % KST, vs = vc % VST;
-          mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
-          uint8_t* kb = sm + OFF_K + ks * (KA + KB);
-          mbar_arrive_expect_tx(&k_full[ks], KA + KB);
-          tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + head, j * BKV, seq);
-          tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + head, j * BKV, seq);
-          if (j == 0) FM_TRACE(1792 + (ul & 63) * 4 + 2);
-          mbar_wait(&v_empty[vs], ((vc / VST) & 1) ^ 1);
-          uint8_t* vb = sm + OFF_V + vs * (VA + VB);
-          mbar_arrive_expect_tx(&v_full[vs], VA + VB);
-          tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + head, j * BKV, seq);
-          tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
-          if (j == nk - 1) FM_TRACE(1792 + (ul & 63) * 4 + 3);
+      };
+      auto load_k = [&](int u, int j) {
+        const int head = (u / pairs) % p.heads, seq = u / (pairs * p.heads);
+        const int ks = kc % KST;
+        mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
+        uint8_t* kb = sm + OFF_K + ks * (KA + KB);
+        mbar_arrive_expect_tx(&k_full[ks], KA + KB);
+        tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + head, j * BKV, seq);
+        tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + head, j * BKV, seq);
+        ++kc;
+      };
+      auto load_v = [&](int u, int j) {
+        const int head = (u / pairs) % p.heads, seq = u / (pairs * p.heads);
+        const int vs = vc % VST;
+        mbar_wait(&v_empty[vs], ((vc / VST) & 1) ^ 1);
+        uint8_t* vb = sm + OFF_V + vs * (VA + VB);
+        mbar_arrive_expect_tx(&v_full[vs], VA + VB);
+        tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + head, j * BKV, seq);
+        tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
+        ++vc;
+      };
+      int ul = 0;
+      if (blockIdx.x < n_units) {
+        load_q(blockIdx.x);
+        load_k(blockIdx.x, 0);
+      }
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
+        FM_TRACE(1792 + (ul & 63) * 4 + 0);
+        for (int j = 1; j < nk; ++j) {
+          load_k(u, j);
+          load_v(u, j - 1);
         }
+        const int un = u + gridDim.x;
+        if (un < n_units) {
+          load_q(un);
+          FM_TRACE(1792 + ((ul + 1) & 63) * 4 + 1);
+          load_k(un, 0);
+          FM_TRACE(1792 + ((ul + 1) & 63) * 4 + 2);
+        }
+        load_v(u, nk - 1);
+        FM_TRACE(1792 + (ul & 63) * 4 + 3);
       }
       pdl_trigger();
     } else if (warp == 1 || warp == 3) {  // ------------------------ MMA issuers, one per group

@@ -1339,7 +1339,10 @@ static int launch_t(const GemmPlan* p, cudaStream_t s) {
 }
 
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
-  switch (p->epi) {
+  // a plan whose exchange was attached after it was built (ddit_request_set_peers sets ep.xch
+  // on the fc2 plans) needs the load / update / store epilogue: its rows go to their owners
+  const int epi = p->epi == EPI_RESID_RED && (p->ep.xch || p->ep.out2) ? EPI_RESID : p->epi;
+  switch (epi) {
     case EPI_QKV: return launch_t<144, EPI_QKV>(p, s);
     case EPI_BF16:
       switch (p->bn) {

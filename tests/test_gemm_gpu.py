@@ -77,21 +77,20 @@ def test_gemm_resid_gate(cuda, bn, N, K):
     assert rel_l2(x1, x0 + a.float() @ w.float().T + bias) < 1e-5
 
 
-@pytest.mark.parametrize("bn,two", [(192, 1), (128, 0), (96, 1), (256, 0)])
-def test_gemm_resid_reduce_matches_load_update_store(cuda, bn, two):
+@pytest.mark.parametrize("bn", [96, 128, 192, 256])
+def test_gemm_resid_reduce_matches_load_update_store(cuda, bn):
     """The reduce-add residual epilogue (TMA reduce into x, nothing loaded) and the TMA load /
     update / store epilogue give bit-identical x (both round acc + b, g * (.), x + (.) in turn),
     which is what keeps DoP-P (whose fc2 exchanges rows) bit-exact with DoP 1."""
     from paper_2506_13497_b200 import kernels, _lib
 
     L = _lib.lib()
-    M, N, K = 2 * 1013, 1152, 1152
+    M, N, K = 2 * 1013, 2304, 1152
     a, w, bias = _inputs(M, N, K, cuda, seed=5)
     x0 = torch.randn(M, N, device=cuda)
     gate = torch.randn(2, N, device=cuda)
     outs = []
     try:
-        L.ddit_set_gemm_2cta(two)
         for red in (0, 1):
             L.ddit_set_resid_reduce(red)
             x = x0.clone()
@@ -99,7 +98,6 @@ def test_gemm_resid_reduce_matches_load_update_store(cuda, bn, two):
             outs.append(x)
     finally:
         L.ddit_set_resid_reduce(1)
-        L.ddit_set_gemm_2cta(1)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
     b = torch.arange(M, device=cuda) // (M // 2)
