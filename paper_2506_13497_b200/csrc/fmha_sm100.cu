@@ -356,18 +356,75 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       // Each softmax group has its own issuing warp (warp 1: group 0, warp 3: group 1), so a
       // group's QK / PV go to the tensor core as soon as ITS softmax is ready, independent of the
       // other group's progress; the shared K / V stages are released by both (count-2 barriers).
+      // The group's tiles form one stream across units: QK_j is issued before PV_{j-1}, and the
+      // next unit's first QK before this unit's last PV, so S of the next unit is ready when the
+      // softmax finishes this unit (its O epilogue runs later, inside the next unit's first tile).
       const int g = warp == 1 ? 0 : 1;
       constexpr uint32_t id_qk = idesc_f16(128, 128, false);
       constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
       constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
       const uint32_t s_tmem = tmem + TM_S0 + 128 * g, o_tmem = tmem + TM_O0 + 128 * g;
       const uint32_t pb = smem_u32(sm + OFF_P + g * PBUF);
-      int kc = 0, vc = 0, qc = 0, sn = 0, pn = 0, un = 0;
+      int kc = 0, vc = 0, qc = 0, sn = 0, pn = 0, un = 0, upv = 0;
+      auto issue_qk = [&](uint32_t qa, int j) {
+        mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
+        if (sn > 0) mbar_wait(&s_free[g], (sn - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t ka = smem_u32(sm + OFF_K + (kc % KST) * (KA + KB)), kb = ka + KA;
+          // ragged last tile: only round16(valid) key columns (the rest of S is never read)
+          const int kv16 = (min(BKV, p.Lk - j * BKV) + 15) & ~15;
+          const uint32_t idq = kv16 == BKV ? id_qk : idesc_f16(128, kv16, false);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ss(s_tmem, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2),
+                         idq, k > 0);
+          umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), idq, 1);
+          umma_commit(&s_full[g]);
+          umma_commit(&k_empty[kc % KST]);
+          FM_TRACE(1024 + g * 256 + (sn & 63) * 2);
+        }
+        __syncwarp();
+        ++sn;
+        ++kc;
+      };
+      // O (+)= P_j V_j once the group wrote P; a unit's first PV overwrites O, so the group's
+      // epilogue must have read the previous unit's O (o_free)
+      auto issue_pv = [&](int j) {
+        if (j == 0) {
+          if (upv > 0) mbar_wait(&o_free[g], (upv - 1) & 1);
+          ++upv;
+        }
+        mbar_wait(&v_ready[vc % VST], (vc / VST) & 1);
+        mbar_wait(&p_full[g], pn & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t va = smem_u32(sm + OFF_V + (vc % VST) * (VA + VB)), vb = va + VA;
+          const int ksteps = (min(BKV, p.Lk - j * BKV) + 15) >> 4;  // 16-key steps with keys
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            if (kk >= ksteps) break;
+            const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+            const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+            umma_bf16_ss(o_tmem, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
+            umma_bf16_ss(o_tmem + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+          }
+          umma_commit(&pv_done[g]);
+          umma_commit(&v_empty[vc % VST]);
+          FM_TRACE(1024 + g * 256 + (pn & 63) * 2 + 1);
+        }
+        __syncwarp();
+        ++pn;
+        ++vc;
+      };
+      int pend = -1;  // tile index (in its unit) of the PV still to issue
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         int pr, head, seq;
         bool has1;
         decode(u, pr, head, seq, has1);
         if (g == 1 && !has1) {  // no second Q tile: keep the shared K / V ring in step
+          if (pend >= 0) issue_pv(pend);  // (its V stage precedes this unit's)
+          pend = -1;
           for (int j = 0; j < nk; ++j, ++kc, ++vc) {
             mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
             if (lane == 0) mbar_arrive(&k_empty[kc % KST]);
@@ -382,62 +439,15 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         if (lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 0);
         mbar_wait(&q_full[qi], (qc >> 1) & 1);
         if (lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 1);
-        for (int j = 0; j <= nk; ++j) {
-          if (j < nk) {  // S = Q K_j^T once the group holds its previous S in registers
-            mbar_wait(&k_full[kc % KST], (kc / KST) & 1);
-            if (j == 0 && lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 2);
-            if (sn > 0) mbar_wait(&s_free[g], (sn - 1) & 1);
-            if (j == 0 && lane == 0) FM_TRACE(1536 + g * 128 + (un & 31) * 4 + 3);
-            tc_fence_after();
-            if (elect_one()) {
-              const uint32_t ka = smem_u32(sm + OFF_K + (kc % KST) * (KA + KB)), kb = ka + KA;
-              // ragged last tile: only round16(valid) key columns (the rest of S is never read)
-              const int kv16 = (min(BKV, p.Lk - j * BKV) + 15) & ~15;
-              const uint32_t idq = kv16 == BKV ? id_qk : idesc_f16(128, kv16, false);
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                umma_bf16_ss(s_tmem, sdesc(qa + 32 * k, 16, 1024, 2), sdesc(ka + 32 * k, 16, 1024, 2),
-                             idq, k > 0);
-              umma_bf16_ss(s_tmem, sdesc(qa + QA, 16, 256, 6), sdesc(kb, 16, 256, 6), idq, 1);
-              umma_commit(&s_full[g]);
-              umma_commit(&k_empty[kc % KST]);
-              FM_TRACE(1024 + g * 256 + (sn & 63) * 2);
-              if (j == nk - 1) umma_commit(&q_empty[qi]);
-            }
-            __syncwarp();
-            ++sn;
-            ++kc;
-          }
-          if (j > 0) {  // O (+)= P_{j-1} V_{j-1} once the group wrote P
-            // the unit's first PV overwrites O: the group must have read its previous O. Only
-            // here -- the unit's first QK already ran during that epilogue
-            if (j == 1 && un > 0) mbar_wait(&o_free[g], (un - 1) & 1);
-            mbar_wait(&v_ready[vc % VST], (vc / VST) & 1);
-            mbar_wait(&p_full[g], pn & 1);
-            tc_fence_after();
-            if (elect_one()) {
-              const uint32_t va = smem_u32(sm + OFF_V + (vc % VST) * (VA + VB)), vb = va + VA;
-              const int ksteps = (min(BKV, p.Lk - (j - 1) * BKV) + 15) >> 4;  // 16-key steps with keys
-#pragma unroll
-              for (int kk = 0; kk < 8; ++kk) {
-                if (kk >= ksteps) break;
-                const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
-                const uint32_t acc = (j > 1 || kk > 0) ? 1u : 0u;
-                umma_bf16_ss(o_tmem, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
-                umma_bf16_ss(o_tmem + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
-              }
-              umma_commit(&pv_done[g]);
-              umma_commit(&v_empty[vc % VST]);
-              FM_TRACE(1024 + g * 256 + (pn & 63) * 2 + 1);
-            }
-            __syncwarp();
-            ++pn;
-            ++vc;
-          }
+        for (int j = 0; j < nk; ++j) {
+          issue_qk(qa, j);
+          if (pend >= 0) issue_pv(pend);
+          pend = j;
         }
         ++qc;
         ++un;
       }
+      if (pend >= 0) issue_pv(pend);
     } else if (warp == 2) {  // ----------------------------------- V fixup (row sums on the TC)
       // head_dim 72 leaves V columns 72..79 of every stage zero (TMA out-of-bounds fill). Writing
       // ones into column 72 makes the PV MMA produce O[:, 72] = sum_k P[:, k]: the softmax row sum
@@ -473,6 +483,55 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
     uint8_t* pbuf = sm + OFF_P + g * PBUF;
     int n = 0;   // tiles processed by this group
     int tk = 0;  // exps phases run under the MUFU token (tiles of units with both groups)
+    int qc = 0;  // units of this group (its Q buffer of unit i is g * 2 + (i & 1))
+    // The O epilogue of a unit is deferred into the next unit's first tile (after its exps), so
+    // it overlaps the other group's exps phase instead of stalling the MUFU turn order. O is
+    // staged in the unit's own Q buffer (its last QK completed before its last PV): once the TMA
+    // store has read it, q_empty hands the buffer back to the producer.
+    int e_qt = 0, e_head = 0, e_seq = 0, e_qi = -1, q_release = -1;
+    auto epilogue = [&]() {
+      mbar_wait(&pv_done[g], (n - 1) & 1);  // the unit's last PV (tile n-1)
+      if (quarter == 0 && lane == 0) FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 5);
+      tc_fence_after();
+      uint32_t o[16];  // columns 64..79: O[64..71], the row sum l (ones column of V) at 72
+      tmem_ld16(o_tm + 64, o);
+      tmem_ld_wait();
+      const float l = __uint_as_float(o[8]);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint8_t* stage = sm + OFF_Q + e_qi * QT;
+      const uint32_t obase = smem_u32(stage) + row * 144;
+      st_shared_u4(obase + 128, pack_bf16(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv),
+                   pack_bf16(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv),
+                   pack_bf16(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv),
+                   pack_bf16(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv));
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t oc[32];
+        tmem_ld32(o_tm + 32 * h, oc);
+        tmem_ld_wait();
+        if (h == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 31) mbar_arrive_relaxed(&o_free[g]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          st_shared_u4(obase + h * 64 + c * 16,
+                       pack_bf16(__uint_as_float(oc[8 * c + 0]) * inv, __uint_as_float(oc[8 * c + 1]) * inv),
+                       pack_bf16(__uint_as_float(oc[8 * c + 2]) * inv, __uint_as_float(oc[8 * c + 3]) * inv),
+                       pack_bf16(__uint_as_float(oc[8 * c + 4]) * inv, __uint_as_float(oc[8 * c + 5]) * inv),
+                       pack_bf16(__uint_as_float(oc[8 * c + 6]) * inv, __uint_as_float(oc[8 * c + 7]) * inv));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+      if (elected) {
+        tma_store_4d(&tmO, stage, 0, p.o_slot + e_head, e_qt * BQ, e_seq);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 6);
+      }
+      q_release = e_qi;
+      e_qi = -1;
+    };
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       int pr, head, seq;
       bool has1;
@@ -597,10 +656,9 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
             }
             tmem_st_wait();
           }
-        } else {
-          // the P buffer staged the previous unit's O store: wait until the TMA read it
-          if (elected) bulk_wait_read0();
-          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        } else if (e_qi >= 0) {
+          // previous unit's O epilogue (its last PV also freed the P buffer)
+          epilogue();
         }
         const uint32_t prow = smem_u32(pbuf) + (uint32_t)(row * 128);
 #pragma unroll
@@ -612,41 +670,21 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         __syncwarp();
         if (lane == 31) mbar_arrive(&p_full[g]);  // release (P stores), from a lane without bulk copies
         if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 4);
+        if (q_release >= 0) {  // the O store has read its staging: the Q buffer goes back
+          if (elected) {
+            bulk_wait_read0();
+            mbar_arrive(&q_empty[q_release]);
+          }
+          q_release = -1;
+        }
       }
-      // ---- unit epilogue: O / l -> bf16 -> staging (the P buffer, 144 B rows) -> TMA store
-      mbar_wait(&pv_done[g], (n - 1) & 1);
-      if (quarter == 0 && lane == 0) FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 5);
-      tc_fence_after();
-      uint32_t o[80];  // columns 0..71: O, column 72: the row sum l (ones column of V)
-      tmem_ld32(o_tm, o);
-      tmem_ld32(o_tm + 32, o + 32);
-      tmem_ld16(o_tm + 64, o + 64);
-      tmem_ld_wait();
-      const float l = __uint_as_float(o[72]);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 31) mbar_arrive_relaxed(&o_free[g]);
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      // the O staging overwrites this group's P buffer: the last PV has read it (pv_done above);
-      // the named barrier also orders every warp's P stores before any O store for the
-      // sanitizer, which does not follow the tcgen05.commit -> mbarrier chain
-      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-      const uint32_t obase = smem_u32(pbuf) + row * 144;
-#pragma unroll
-      for (int c = 0; c < 9; ++c)
-        st_shared_u4(obase + c * 16,
-                     pack_bf16(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
-                     pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
-                     pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
-                     pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-      if (elected) {
-        tma_store_4d(&tmO, pbuf, 0, p.o_slot + head, qt * BQ, seq);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        FM_TRACE(g * 512 + ((n - 1) & 63) * 8 + 6);
-      }
+      e_qt = qt;
+      e_head = head;
+      e_seq = seq;
+      e_qi = g * 2 + (qc & 1);
+      ++qc;
     }
+    if (e_qi >= 0) epilogue();
     if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();

@@ -119,23 +119,26 @@ def test_tiny_step_matches_golden_fixture(cuda, step):
     assert rel_l2(out, ref) <= 1e-2 and rel_l2(out - z, ref - z) <= 2e-2
 
 
-def test_tc_and_mma_attention_paths_agree(cuda):
-    """The tcgen05 FMHA (default) and the mma.sync flash kernel give the same step."""
-    from paper_2506_13497_b200 import shapes, weights
+def test_step_has_one_attention_path(cuda):
+    """Spatial / cross attention always run the tcgen05 FMHA: the retired option that selected
+    the mma.sync flash kernel is refused (no silent second backend on the step path)."""
+    from paper_2506_13497_b200._lib import DditError
+    from paper_2506_13497_b200 import weights
     from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
 
     cfg = dataclasses.replace(weights.XL2, depth=1)
     W, sh, z, y = _setup(cfg, "240p")
     model = STDiTModel(cfg, W, cuda)
-    outs = []
-    for tc in (1, 0):
-        req = StepRequest(model, sh, y.to(cuda))
-        req.set_option(1, tc)
-        zd = z.to(cuda).contiguous()
-        req.step(zd, 3)
-        torch.cuda.synchronize()
-        outs.append(zd.cpu())
-    assert rel_l2(outs[0] - z, outs[1] - z) < 5e-3
+    req = StepRequest(model, sh, y.to(cuda))
+    with pytest.raises(DditError):
+        req.set_option(1, 0)
+    req.set_option(1, 1)  # accepted (the only path)
+    zd = z.to(cuda).contiguous()
+    req.step(zd, 3)
+    torch.cuda.synchronize()
+    assert torch.isfinite(zd).all()
+    req.close()
+    model.close()
 
 
 def test_graph_replay_matches_eager(cuda):
