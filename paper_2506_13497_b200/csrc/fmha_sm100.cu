@@ -207,11 +207,49 @@ DDIT_DEV float2 exp2_poly_x2(float x0, float x1) {
 // POLY-th chunk (POLY = 0: none)
 template <int POLY>
 __host__ __device__ constexpr bool poly_chunk(int c) { return POLY > 0 && c % POLY == POLY - 1; }
+// 1 / x for x > 0 on the FMA pipe (bit-trick seed + 3 Newton steps, rel. err ~1e-7): MUFU.RCP
+// would queue behind the other softmax group's exps
+DDIT_DEV float rcp_fma(float x) {
+  float r = __int_as_float(0x7EF311C7 - __float_as_int(x));
+  r = r * fmaf(-x, r, 2.f);
+  r = r * fmaf(-x, r, 2.f);
+  r = r * fmaf(-x, r, 2.f);
+  return r;
+}
 DDIT_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// Work-unit walk of a persistent CTA: unit u = blockIdx.x, +gridDim.x, ... decomposed as
+// (q-tile pair fastest, head, sequence) -- pair fastest so concurrent CTAs share K/V in L2. The
+// coordinates advance by a mixed-radix add: no integer division inside the loops (it would go
+// through MUFU.RCP, queued behind the other softmax group's exps).
+struct UnitWalk {
+  int u, pr, head, seq;
+  int G, pairs, heads, d_pr, d_head, d_seq;
+  DDIT_DEV UnitWalk(int pairs_, int heads_) : pairs(pairs_), heads(heads_) {
+    G = gridDim.x;
+    u = blockIdx.x;
+    pr = u % pairs;
+    head = (u / pairs) % heads;
+    seq = u / (pairs * heads);
+    d_pr = G % pairs;
+    d_head = (G / pairs) % heads;
+    d_seq = G / (pairs * heads);
+  }
+  DDIT_DEV void next() {
+    u += G;
+    pr += d_pr;
+    int c = pr >= pairs;
+    pr -= c ? pairs : 0;
+    head += d_head + c;
+    c = head >= heads;
+    head -= c ? heads : 0;
+    seq += d_seq + c;
+  }
+};
 
 template <int POLY>
 __global__ void __launch_bounds__(fm::THREADS, 1)
@@ -278,13 +316,12 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
 
-  // unit -> (q-tile pair, head, sequence); pair fastest so concurrent CTAs share K/V in L2
-  auto decode = [&](int u, int& pr, int& head, int& seq, bool& has1) {
-    pr = u % pairs;
-    head = (u / pairs) % p.heads;
-    seq = u / (pairs * p.heads);
-    has1 = 2 * pr + 1 < p.q_tiles;
-  };
+  // unit -> (q-tile pair, head, sequence): see UnitWalk; each role builds its own walker after
+  // its setmaxnreg, so the walk state is not live across the role split
+  auto first = [&]() { return UnitWalk(pairs, p.heads); };
+  auto advance = [](UnitWalk& w) { w.next(); };
+  using Walk = UnitWalk;
+  auto has_second = [&](const Walk& w) { return 2 * w.pr + 1 < p.q_tiles; };
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
@@ -294,10 +331,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       // never queues behind a V stage that frees only after a later softmax phase: the next
       // unit's first QK can issue right after this unit's last PV.
       int kc = 0, vc = 0, qc[2] = {0, 0};
-      auto load_q = [&](int u) {
-        int pr, head, seq;
-        bool has1;
-        decode(u, pr, head, seq, has1);
+      auto load_q = [&](const Walk& w) {
+        const bool has1 = has_second(w);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if (g == 1 && !has1) break;
@@ -305,51 +340,52 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           mbar_wait(&q_empty[qi], ((qc[g] >> 1) & 1) ^ 1);
           uint8_t* qbuf = sm + OFF_Q + qi * QT;
           mbar_arrive_expect_tx(&q_full[qi], QT);
-          tma_load_4d(qbuf, &tmQa, &q_full[qi], 0, p.q_slot + head, (2 * pr + g) * BQ, seq);
-          tma_load_4d(qbuf + QA, &tmQb, &q_full[qi], 64, p.q_slot + head, (2 * pr + g) * BQ, seq);
+          tma_load_4d(qbuf, &tmQa, &q_full[qi], 0, p.q_slot + w.head, (2 * w.pr + g) * BQ, w.seq);
+          tma_load_4d(qbuf + QA, &tmQb, &q_full[qi], 64, p.q_slot + w.head, (2 * w.pr + g) * BQ, w.seq);
           ++qc[g];
         }
       };
-      auto load_k = [&](int u, int j) {
-        const int head = (u / pairs) % p.heads, seq = u / (pairs * p.heads);
+      auto load_k = [&](const Walk& w, int j) {
         const int ks = kc % KST;
         mbar_wait(&k_empty[ks], ((kc / KST) & 1) ^ 1);
         uint8_t* kb = sm + OFF_K + ks * (KA + KB);
         mbar_arrive_expect_tx(&k_full[ks], KA + KB);
-        tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + head, j * BKV, seq);
-        tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + head, j * BKV, seq);
+        tma_load_4d(kb, &tmKVa, &k_full[ks], 0, p.k_slot + w.head, j * BKV, w.seq);
+        tma_load_4d(kb + KA, &tmKVb, &k_full[ks], 64, p.k_slot + w.head, j * BKV, w.seq);
         ++kc;
       };
-      auto load_v = [&](int u, int j) {
-        const int head = (u / pairs) % p.heads, seq = u / (pairs * p.heads);
+      auto load_v = [&](const Walk& w, int j) {
         const int vs = vc % VST;
         mbar_wait(&v_empty[vs], ((vc / VST) & 1) ^ 1);
         uint8_t* vb = sm + OFF_V + vs * (VA + VB);
         mbar_arrive_expect_tx(&v_full[vs], VA + VB);
-        tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + head, j * BKV, seq);
-        tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + head, j * BKV, seq);
+        tma_load_4d(vb, &tmKVa, &v_full[vs], 0, p.v_slot + w.head, j * BKV, w.seq);
+        tma_load_4d(vb + VA, &tmKVb, &v_full[vs], 64, p.v_slot + w.head, j * BKV, w.seq);
         ++vc;
       };
       int ul = 0;
-      if (blockIdx.x < n_units) {
-        load_q(blockIdx.x);
-        load_k(blockIdx.x, 0);
+      Walk w = first();
+      if (w.u < n_units) {
+        load_q(w);
+        load_k(w, 0);
       }
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
+      for (; w.u < n_units; ++ul) {
         FM_TRACE(1792 + (ul & 63) * 4 + 0);
         for (int j = 1; j < nk; ++j) {
-          load_k(u, j);
-          load_v(u, j - 1);
+          load_k(w, j);
+          load_v(w, j - 1);
         }
-        const int un = u + gridDim.x;
-        if (un < n_units) {
-          load_q(un);
+        Walk wn = w;
+        advance(wn);
+        if (wn.u < n_units) {
+          load_q(wn);
           FM_TRACE(1792 + ((ul + 1) & 63) * 4 + 1);
-          load_k(un, 0);
+          load_k(wn, 0);
           FM_TRACE(1792 + ((ul + 1) & 63) * 4 + 2);
         }
-        load_v(u, nk - 1);
+        load_v(w, nk - 1);
         FM_TRACE(1792 + (ul & 63) * 4 + 3);
+        w = wn;
       }
       pdl_trigger();
     } else if (warp == 1 || warp == 3) {  // ------------------------ MMA issuers, one per group
@@ -418,11 +454,8 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         ++vc;
       };
       int pend = -1;  // tile index (in its unit) of the PV still to issue
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int pr, head, seq;
-        bool has1;
-        decode(u, pr, head, seq, has1);
-        if (g == 1 && !has1) {  // no second Q tile: keep the shared K / V ring in step
+      for (Walk w = first(); w.u < n_units; advance(w)) {
+        if (g == 1 && !has_second(w)) {  // no second Q tile: keep the shared K / V ring in step
           if (pend >= 0) issue_pv(pend);  // (its V stage precedes this unit's)
           pend = -1;
           for (int j = 0; j < nk; ++j, ++kc, ++vc) {
@@ -455,15 +488,18 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       // softmax warps drop their per-element sum. Column 72 = element 8 of the 16-column SW32
       // tail: 16 B chunk 1 of each 32 B row, swizzled with bit 2 of the row.
       int vc = 0;
+      const uint32_t tail0 = smem_u32(sm + OFF_V + VA);
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         for (int j = 0; j < nk; ++j, ++vc) {
           const int vs = vc % VST;
           mbar_wait(&v_full[vs], (vc / VST) & 1);
-          uint8_t* tail = sm + OFF_V + vs * (VA + VB) + VA;
+          const uint32_t tail = tail0 + vs * (VA + VB);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r = lane + 32 * i;
-            *reinterpret_cast<uint16_t*>(tail + r * 32 + (((r >> 2) & 1) ? 0 : 16)) = 0x3F80;  // bf16 1.0
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(tail + r * 32 + (((r >> 2) & 1) ? 0 : 16)),
+                         "h"((unsigned short)0x3F80)
+                         : "memory");  // bf16 1.0
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -497,7 +533,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       tmem_ld16(o_tm + 64, o);
       tmem_ld_wait();
       const float l = __uint_as_float(o[8]);
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const float inv = l > 0.f ? rcp_fma(l) : 0.f;
       uint8_t* stage = sm + OFF_Q + e_qi * QT;
       const uint32_t obase = smem_u32(stage) + row * 144;
       st_shared_u4(obase + 128, pack_bf16(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv),
@@ -532,16 +568,15 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       q_release = e_qi;
       e_qi = -1;
     };
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int pr, head, seq;
-      bool has1;
-      decode(u, pr, head, seq, has1);
+    for (Walk w = first(); w.u < n_units; advance(w)) {
+      const bool has1 = has_second(w);
       if (g == 1 && !has1) continue;
-      const int qt = 2 * pr + g;
+      const int qt = 2 * w.pr + g, head = w.head, seq = w.seq;
       float m = -INFINITY;
       for (int j = 0; j < nk; ++j, ++n) {
-        mbar_wait(&s_full[g], n & 1);
         const bool trc = quarter == 0 && lane == 0;
+        if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 7);
+        mbar_wait(&s_full[g], n & 1);
         if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 0);
         tc_fence_after();
         uint32_t s[128];

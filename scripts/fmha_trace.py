@@ -54,11 +54,11 @@ def rel(x):
     return (x - t0) if x else -1
 
 
-names = ["S_rdy", "tok", "exps", "Pfree", "Pst", "O_rdy", "O_st"]
+names = ["S_wait", "S_rdy", "tok", "exps", "Pfree", "Pst", "O_rdy", "O_st"]
 for grp in (0, 1):
     print(f"softmax group {grp}: tile: " + " ".join(f"{n:>7}" for n in names) + "   QKiss   PViss")
     for n in range(64):
-        row = [rel(v[grp * 512 + n * 8 + k]) for k in range(7)]
+        row = [rel(v[grp * 512 + n * 8 + 7])] + [rel(v[grp * 512 + n * 8 + k]) for k in range(7)]
         mm = [rel(v[1024 + grp * 256 + n * 2 + k]) for k in range(2)]
         if row[0] < 0 and mm[0] < 0:
             continue
