@@ -113,6 +113,15 @@ DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
 /* Short-sequence (T <= 32) temporal attention: q/k/v must be the three sections of one
  * row-major QKV matrix and share one index map; one CTA per (batch, token position). */
 DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
+/* LayerNorm (no affine, eps) + t2i modulate of the fp32 residual rows:
+ * out_bf16[r, :] = LN(x[r, :]) * (1 + scale[b]) + shift[b], b = r / rows_per_b, shift / scale
+ * rows mod_stride floats apart. The step's own LN launch (same kernel). */
+DDIT_API int ddit_ln_modulate(const float* x, void* out_bf16, int M, int C, const float* shift,
+                              const float* scale, int mod_stride, int rows_per_b, float eps,
+                              void* stream);
+/* LN kernel variant for launches made afterwards (tuning): 1 one warp per row, 3 (default)
+ * persistent streaming warps (C = 1152; other widths take the generic kernel). Env DDIT_LN. */
+DDIT_API int ddit_set_ln_variant(int variant);
 /* tcgen05 / TMEM flash attention (spatial and cross attention): contiguous sequences
  * (tok == 1, inner <= 1), row strides and head offsets in whole 72-column slots, k and v in one
  * matrix. Returns DDIT_E_INVALID for layouts it does not cover. */

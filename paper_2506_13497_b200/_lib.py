@@ -134,6 +134,8 @@ _SIGNATURES = {
     "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
     "ddit_attention_tc": [ctypes.POINTER(Attn), vp],
+    "ddit_ln_modulate": [vp, vp, ci, ci, vp, vp, ci, ci, ctypes.c_float, vp],
+    "ddit_set_ln_variant": [ci],
     "ddit_model_create": [ctypes.POINTER(CConfig), ctypes.POINTER(CWeights), ctypes.POINTER(vp)],
     "ddit_request_workspace_bytes": [vp, ctypes.POINTER(CReqDesc), ctypes.POINTER(ctypes.c_uint64)],
     "ddit_request_shard": [vp, ctypes.POINTER(CReqDesc)] + [ctypes.POINTER(ci)] * 4,

@@ -6,6 +6,7 @@
 #include "ddit.h"
 #include "capi_internal.h"
 #include "gemm_sm100.cuh"
+#include "elementwise.cuh"
 
 namespace ddit {
 static thread_local char g_capi_err[1024] = "";
@@ -74,6 +75,28 @@ DDIT_API int ddit_enable_peer_access(int device, int peer) {
 }
 DDIT_API int ddit_set_pdl(int on) {
   set_pdl(on);
+  return DDIT_OK;
+}
+DDIT_API int ddit_ln_modulate(const float* x, void* out_bf16, int M, int C, const float* shift,
+                              const float* scale, int mod_stride, int rows_per_b, float eps,
+                              void* stream) {
+  if (!x || !out_bf16 || !shift || !scale) {
+    set_error("ddit_ln_modulate: null argument");
+    return DDIT_E_INVALID;
+  }
+  if (ln_modulate(x, static_cast<__nv_bfloat16*>(out_bf16), M, C, shift, scale, mod_stride,
+                  rows_per_b, eps, static_cast<cudaStream_t>(stream))) {
+    set_error("ddit_ln_modulate: unsupported shape M=%d C=%d", M, C);
+    return DDIT_E_INVALID;
+  }
+  return check_cuda("ln_modulate");
+}
+DDIT_API int ddit_set_ln_variant(int variant) {
+  if (variant != 0 && variant != 1 && variant != 2 && variant != 3) {
+    set_error("ddit_set_ln_variant: unknown variant %d", variant);
+    return DDIT_E_INVALID;
+  }
+  set_ln_variant(variant);
   return DDIT_OK;
 }
 DDIT_API int ddit_set_resid_reduce(int on) {

@@ -134,14 +134,17 @@ __global__ void __launch_bounds__(256)
 }
 
 static int g_ln_variant = -1;  // tuning hook (env DDIT_LN): 0 generic, 1 = 32 lanes x 9, 2 = 16 x 18,
+                               // 3 (default; 240p: 12 vs 17 us hot, 14 vs 19 cold, scripts/ln_bench.py)
                                // 3 = persistent streaming warps
+
+void set_ln_variant(int v) { g_ln_variant = v; }
 
 int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
                 const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s) {
   if (C % 4 || C > 32 * 4 * kMaxVec || M <= 0) return -2;
   if (g_ln_variant < 0) {
     const char* e = getenv("DDIT_LN");
-    g_ln_variant = e ? atoi(e) : 1;
+    g_ln_variant = e ? atoi(e) : 3;
   }
   const int rpb = rows_per_b > 0 ? rows_per_b : M;
   if (C == 1152 && g_ln_variant == 3) {

@@ -5,6 +5,7 @@
 #include <stddef.h>
 
 namespace ddit {
+void set_ln_variant(int v);
 int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* shift,
                 const float* scale, int mod_stride, int rows_per_b, float eps, cudaStream_t s);
 int timestep_freq(float* freq, const float* tvals, int nvals, int dim, cudaStream_t s);

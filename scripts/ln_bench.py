@@ -1,0 +1,68 @@
+"""LN + modulate at the 240p step shape (M = 12150 rows x C = 1152, fp32 in, bf16 out) per kernel
+variant, graph-replayed, interleaved in one process; torch's fp32 -> bf16 cast of the same tensor
+(same bytes: 4 B read + 2 B written per element) as the practical HBM roofline of this stream.
+x hot = one buffer (L2 resident after the first call), cold = 4 rotating buffers (224 MB > L2)."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+from paper_2506_13497_b200 import _lib
+
+L = _lib.lib()
+dev = torch.device("cuda:0")
+M, C = 12150, 1152
+xs = [torch.randn(M, C, device=dev) for _ in range(4)]
+out = torch.empty(M, C, device=dev, dtype=torch.bfloat16)
+mods = torch.randn(2, 6, C, device=dev)
+shift, scale = mods[:, 0], mods[:, 1]
+
+
+def ln(x):
+    _lib.check(L.ddit_ln_modulate(x.data_ptr(), out.data_ptr(), M, C, shift.data_ptr(), scale.data_ptr(),
+                                  6 * C, M // 2, 1e-6, torch.cuda.current_stream().cuda_stream))
+
+
+def gtime(fn, it=40):
+    for i in range(3):
+        fn(i)
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(it):
+                fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(3):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / (3 * it) * 1e3
+
+
+# correctness of every variant against torch
+ref = torch.nn.functional.layer_norm(xs[0], (C,), eps=1e-6)
+b = torch.arange(M, device=dev) // (M // 2)
+ref = (ref * (1 + scale[b]) + shift[b]).bfloat16()
+for v in (1, 3):
+    L.ddit_set_ln_variant(v)
+    ln(xs[0])
+    torch.cuda.synchronize()
+    err = (out.float() - ref.float()).abs().max().item()
+    print(f"variant {v}: max |err| vs torch {err:.3e}")
+byt = M * C * 6
+for rnd in range(2):
+    for v in (1, 3):
+        L.ddit_set_ln_variant(v)
+        th = gtime(lambda i: ln(xs[0]))
+        tc = gtime(lambda i: ln(xs[i % 4]))
+        print(f"LN variant {v}: hot {th:6.1f} us ({byt / th / 1e3:6.0f} GB/s)  cold {tc:6.1f} us ({byt / tc / 1e3:6.0f} GB/s)")
+    th = gtime(lambda i: out.copy_(xs[0]))
+    tc = gtime(lambda i: out.copy_(xs[i % 4]))
+    print(f"torch cast   : hot {th:6.1f} us ({byt / th / 1e3:6.0f} GB/s)  cold {tc:6.1f} us ({byt / tc / 1e3:6.0f} GB/s)")
+L.ddit_set_ln_variant(3)
