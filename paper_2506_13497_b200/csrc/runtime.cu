@@ -26,9 +26,9 @@
 #include "gemm_sm100.cuh"
 
 #include "fmha_plan.cuh"
+#include "temporal_plan.cuh"
 namespace ddit {
 int attention_launch(const ddit_attn* a, cudaStream_t s);
-int temporal_attention_launch(const ddit_attn* a, cudaStream_t s);
 }
 
 using namespace ddit;
@@ -153,6 +153,8 @@ struct ddit_req {
   std::vector<FmhaPlan> fm_self;   // [2*depth] tcgen05 self-attention plans (spatial blocks)
   std::vector<FmhaPlan> fm_cross;  // [2*depth] tcgen05 cross-attention plans
   std::vector<uint8_t> fm_self_ok, fm_cross_ok;
+  std::vector<TemporalPlan> tm_self;  // [2*depth] tcgen05 temporal-attention plans (T <= 32)
+  std::vector<uint8_t> tm_self_ok;
   PeerPtrs peer_sp{}, peer_tp{};
   PeerFlags peer_flags{};
   bool peers_set = false;
@@ -358,9 +360,14 @@ int ln_mod(ddit_req* r, float* x, int M, const float* shift, const float* scale,
 int attn(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
   return timed(r, K_ATTN, s, 1, [&] { return attention_launch(a, s); });
 }
-int attn_temporal(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
+int attn_temporal(ddit_req* r, int k, const ddit_attn* a, cudaStream_t s) {
   if (a->Lq > 32) return attn(r, a, s);
-  return timed(r, K_ATTN, s, 1, [&] { return temporal_attention_launch(a, s); });
+  if (!r->tm_self_ok[k]) {
+    set_error("block %d: temporal attention plan missing", k);
+    return DDIT_E_CONFIG;
+  }
+  const TemporalPlan& tp = r->tm_self[k];
+  return timed(r, K_ATTN, s, 1, [&] { return temporal_plan_launch(&tp, s); });
 }
 
 // Self-attention index map of block k (spatial: frames are sequences; temporal: positions).
@@ -433,6 +440,8 @@ int build_attn_plans(ddit_req* r) {
   r->fm_cross.assign(nblk, FmhaPlan{});
   r->fm_self_ok.assign(nblk, 0);
   r->fm_cross_ok.assign(nblk, 0);
+  r->tm_self.assign(nblk, TemporalPlan{});
+  r->tm_self_ok.assign(nblk, 0);
   for (int k = 0; k < nblk; ++k) {
     const int M = (k & 1) ? r->g.M_tp : r->g.M_sp;
     if (M == 0) continue;
@@ -441,6 +450,11 @@ int build_attn_plans(ddit_req* r) {
       int rc = fmha_plan_init(&r->fm_self[k], &a);
       if (rc) return rc;
       r->fm_self_ok[k] = 1;
+    }
+    if ((k & 1) && a.Lq <= 32) {
+      int rc = temporal_plan_init(&r->tm_self[k], &a);
+      if (rc) return rc;
+      r->tm_self_ok[k] = 1;
     }
     a = cross_attn_args(r, k);
     if (fmha_supported(&a)) {
@@ -458,7 +472,7 @@ int build_attn_plans(ddit_req* r) {
 int run_attn(ddit_req* r, int k, bool cross, cudaStream_t s) {
   if (!cross && (k & 1)) {
     ddit_attn a = self_attn_args(r, k);
-    return attn_temporal(r, &a, s);
+    return attn_temporal(r, k, &a, s);
   }
   const std::vector<uint8_t>& ok = cross ? r->fm_cross_ok : r->fm_self_ok;
   if (!ok[k]) {

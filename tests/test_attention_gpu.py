@@ -57,6 +57,29 @@ def test_temporal(cuda, B, T, Sl, fast):
     assert e < 1e-2
 
 
+@pytest.mark.parametrize("heads", [4, 12, 20])
+@pytest.mark.parametrize("T", [15, 30])
+def test_temporal_head_counts(cuda, heads, T):
+    """The tcgen05 temporal kernel stacks 128 / R heads per tile (8 at T <= 16, 4 at T <= 32):
+    head counts below one group (4 at T=15), and a partial last group (12, 20 at T=15; none at
+    T=30), against torch fp32."""
+    from paper_2506_13497_b200 import kernels
+    g = torch.Generator().manual_seed(3)
+    B, Sl = 2, 37
+    C = heads * D
+    M = B * T * Sl
+    qkv = torch.randn(M, 3 * C, generator=g).to(cuda, torch.bfloat16)
+    o = torch.full((M, C), float("nan"), device=cuda, dtype=torch.bfloat16)
+    mp = (Sl, T * Sl, 1, Sl)
+    kernels.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, heads=heads, num_seqs=B * Sl,
+                      Lq=T, Lk=T, q_map=mp, kv_map=mp, temporal=True)
+    x = qkv.view(B, T, Sl, 3, heads, D).transpose(1, 2).reshape(B * Sl, T, 3, heads, D)
+    q, k, v = x.unbind(2)
+    ref = ref_attn(q, k, v).reshape(B, Sl, T, C).transpose(1, 2).reshape(M, C)
+    assert not torch.isnan(o).any()
+    assert rel_l2(o, ref) < 1e-2
+
+
 @pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("B,N,Ly", [(2, 777, 300), (2, 64, 300), (1, 100, 17), (2, 6075, 300)])
 def test_cross(cuda, B, N, Ly, tc):
