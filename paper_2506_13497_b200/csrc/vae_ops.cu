@@ -143,24 +143,29 @@ __global__ void __launch_bounds__(256)
           q += r.y;
         }
       }
-      partial[(size_t)c * G + g] = make_float2(s, q);
+      // [n][g][blk]: the finalize reads a group's partials as one contiguous run
+      partial[((size_t)(c / nblk) * G + g) * nblk + c % nblk] = make_float2(s, q);
     }
     __syncthreads();  // red reused by the next chunk
   }
 }
 
+// grid (N, G / 8): one warp per (sample, group); a group's partials are contiguous, so the
+// lanes' loads coalesce (the [n][blk][g] layout made them 256 B-strided: 15 us per call on one SM)
 __global__ void __launch_bounds__(256)
     gn_finalize_kernel(const float2* __restrict__ partial, float2* __restrict__ coef,
                        const float* __restrict__ gamma, const float* __restrict__ beta, int P,
                        int C, int G, int nblk, float eps) {
   const int n = blockIdx.x;
-  __shared__ double mean_s[32], rstd_s[32];
-  // one warp per group: lanes take blocks lane, lane+32, ... then a fixed xor tree (deterministic)
-  const int lane = threadIdx.x & 31;
-  for (int g = threadIdx.x >> 5; g < G; g += blockDim.x >> 5) {
+  __shared__ double mean_s[8], rstd_s[8];
+  // lanes take blocks lane, lane+32, ... then a fixed xor tree (deterministic)
+  const int lane = threadIdx.x & 31, wg = threadIdx.x >> 5;
+  const int g = blockIdx.y * 8 + wg;
+  if (g < G) {
     double s = 0, q = 0;
+    const float2* pg = partial + ((size_t)n * G + g) * nblk;
     for (int b = lane; b < nblk; b += 32) {
-      const float2 v = partial[((size_t)n * nblk + b) * G + g];
+      const float2 v = pg[b];
       s += v.x;
       q += v.y;
     }
@@ -172,15 +177,16 @@ __global__ void __launch_bounds__(256)
       const double cnt = (double)P * (C / G);
       const double mean = s / cnt;
       const double var = fmax(q / cnt - mean * mean, 0.0);
-      mean_s[g] = mean;
-      rstd_s[g] = (double)rsqrtf((float)var + eps);
+      mean_s[wg] = mean;
+      rstd_s[wg] = (double)rsqrtf((float)var + eps);
     }
   }
   __syncthreads();
   const int cg = C / G;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const double a = rstd_s[c / cg] * (double)gamma[c];
-    coef[(size_t)n * C + c] = make_float2((float)a, (float)((double)beta[c] - mean_s[c / cg] * a));
+  const int c0 = blockIdx.y * 8 * cg, c1 = min(C, c0 + 8 * cg);
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double a = rstd_s[(c - c0) / cg] * (double)gamma[c];
+    coef[(size_t)n * C + c] = make_float2((float)a, (float)((double)beta[c] - mean_s[(c - c0) / cg] * a));
   }
 }
 
@@ -458,7 +464,7 @@ extern "C" {
 DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
                             const float* beta, int N, int P, int C, int G, float eps, int silu_act,
                             void* stream) {
-  // `stats` scratch layout: fp64 [N][G][2] followed by the fp32x2 partials [N][nblk][G]
+  // `stats` scratch layout: fp64 [N][G][2] followed by the fp32x2 partials [N][G][nblk]
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (C % 8 || C % G || G > 32 || (C / 8) > 256 || 256 % (C / 8)) {
     set_error("groupnorm: C a power of two in [8, 2048] divisible by G <= 32 required");
@@ -486,7 +492,7 @@ DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* 
   const int pgrid = std::max(1, std::min(N * nblk, 3 * sms[dev]));  // persistent, 3 per SM
   gn_partial_kernel<<<pgrid, 256, kGnPartSmem, s>>>(static_cast<const __nv_bfloat16*>(x), partial, N,
                                                     P, C, G, ppb, nblk);
-  gn_finalize_kernel<<<N, 256, 0, s>>>(partial, coef, gamma, beta, P, C, G, nblk, eps);
+  gn_finalize_kernel<<<dim3(N, (G + 7) / 8), 256, 0, s>>>(partial, coef, gamma, beta, P, C, G, nblk, eps);
   const size_t vpn = (size_t)P * (C / 8);
   const dim3 grid((unsigned)((vpn + 256 * kGnUnroll - 1) / (256 * kGnUnroll)), N);
   if (silu_act)
