@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(ta::THREADS, 1)
       ta::st_shared_u4(smem_u32(sm) + op * OPND + (c < 8 ? r * 128 + c * 16 : BOXA + r * 32 + (((r >> 2) & 1) << 4)),
                        0u, 0u, 0u, 0u);
     }
+    asm volatile("bar.sync 2, 128;" ::: "memory");  // zeros in place before any copy lands
     // a (operand, frame) run of a unit is HG head slices of 144 B = CH 16 B chunks, contiguous in
     // the QKV row; lane chunk j of a run is chunk lane + 32 j (head i_j, column chunk c_j)
     constexpr int CH = 9 * HG, NJ = (CH + 31) / 32;
