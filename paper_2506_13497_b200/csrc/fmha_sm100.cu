@@ -24,7 +24,7 @@
 //                 tile's P buffer) -> TMA store.
 // Persistent: grid = #SMs, each CTA walks units (q-tile pair fastest, so concurrent CTAs share
 // K/V in L2); Q is double-buffered per softmax group, K and V stream through their own rings
-// across units. TMEM: S0 [0,128), S1 [128,256), O0 [256,336), O1 [384,464).
+// across units. TMEM: S0 [0,128), S1 [128,256), O0 [256,336), O1 [336,416), P0 [416,464), P1 [464,512).
 #include "common.cuh"
 #include "ddit.h"
 #include "capi_internal.h"
@@ -64,7 +64,18 @@ constexpr int OFF_P = OFF_V + VST * (VA + VB);     // P per group (also its O st
 constexpr int OFF_BAR = OFF_P + 2 * PBUF;
 constexpr int NBAR = 32;
 constexpr int SMEM = 1024 + OFF_BAR + NBAR * 8 + 16;
-constexpr uint32_t TM_S0 = 0, TM_O0 = 256;  // group g: S at TM_S0 + 128 g, O at TM_O0 + 128 g
+#ifndef DDIT_FMHA_PTMEM
+#define DDIT_FMHA_PTMEM 1
+#endif
+#if DDIT_FMHA_PTMEM
+// group g: S at TM_S0 + 128 g, O at TM_O0 + 80 g, keys 0..95 of P (bf16, two per column) at
+// TM_P0 + 48 g; keys 96..127 of P stay in shared memory
+constexpr uint32_t TM_S0 = 0, TM_O0 = 256, TM_OSTEP = 80, TM_P0 = 416, TM_PSTEP = 48;
+constexpr int P_TM_CHUNKS = 12;  // 8-key chunks of P held in TMEM
+#else
+constexpr uint32_t TM_S0 = 0, TM_O0 = 256, TM_OSTEP = 128;  // group g: S at TM_S0 + 128 g, O at TM_O0 + 128 g
+constexpr int P_TM_CHUNKS = 0;
+#endif
 constexpr float RESCALE_LOG2 = 8.0f;
 static_assert(SMEM <= 232448, "fmha smem");
 }  // namespace fm
@@ -93,6 +104,15 @@ DDIT_DEV uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layo
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)layout << 61;
   return d;
+}
+// D[tmem] (+)= A[tmem] * B[smem] (A: M x 16 bf16, two per 32-bit TMEM column)
+DDIT_DEV void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn_major ? (1u << 16) : 0u) |
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
       constexpr uint32_t id_qk = idesc_f16(128, 128, false);
       constexpr uint32_t id_pv64 = idesc_f16(128, 64, true);
       constexpr uint32_t id_pv16 = idesc_f16(128, 16, true);
-      const uint32_t s_tmem = tmem + TM_S0 + 128 * g, o_tmem = tmem + TM_O0 + 128 * g;
+      const uint32_t s_tmem = tmem + TM_S0 + 128 * g, o_tmem = tmem + TM_O0 + TM_OSTEP * g;
       const uint32_t pb = smem_u32(sm + OFF_P + g * PBUF);
       int kc = 0, vc = 0, qc = 0, sn = 0, pn = 0, un = 0, upv = 0;
       auto issue_qk = [&](uint32_t qa, int j) {
@@ -440,8 +460,16 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             if (kk >= ksteps) break;
-            const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
             const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+#if DDIT_FMHA_PTMEM
+            if (kk < P_TM_CHUNKS / 2) {  // P keys 16 kk .. 16 kk + 15 from TMEM (A operand in TMEM)
+              const uint32_t pa = tmem + TM_P0 + TM_PSTEP * g + 8 * kk;
+              umma_ts(o_tmem, pa, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
+              umma_ts(o_tmem + 64, pa, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
+              continue;
+            }
+#endif
+            const uint64_t a = sdesc(pb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
             umma_bf16_ss(o_tmem, a, sdesc(va + kk * 2048, 8192, 1024, 2), id_pv64, acc);
             umma_bf16_ss(o_tmem + 64, a, sdesc(vb + kk * 512, 8192, 256, 6), id_pv16, acc);
           }
@@ -513,7 +541,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_tm = lane_base + TM_S0 + 128 * g, o_tm = lane_base + TM_O0 + 128 * g;
+    const uint32_t s_tm = lane_base + TM_S0 + 128 * g, o_tm = lane_base + TM_O0 + TM_OSTEP * g;
     const int bar_id = 1 + g;
     const bool elected = quarter == 0 && lane == 0;
     uint8_t* pbuf = sm + OFF_P + g * PBUF;
@@ -696,11 +724,20 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           epilogue();
         }
         const uint32_t prow = smem_u32(pbuf) + (uint32_t)(row * 128);
+#if DDIT_FMHA_PTMEM
+        // chunks 0..11 (keys 0..95) -> TMEM columns (two bf16 per column), issued first
+        tmem_st16(lane_base + TM_P0 + TM_PSTEP * g, s);
+        tmem_st16(lane_base + TM_P0 + TM_PSTEP * g + 16, s + 16);
+        tmem_st16(lane_base + TM_P0 + TM_PSTEP * g + 32, s + 32);
+#endif
 #pragma unroll
-        for (int c = 0; c < 16; ++c)  // chunk c (8 keys) -> region c / 8, 16 B swizzled
+        for (int c = P_TM_CHUNKS; c < 16; ++c)  // chunk c (8 keys) -> region c / 8, 16 B swizzled
           st_shared_u4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), s[4 * c], s[4 * c + 1],
                        s[4 * c + 2], s[4 * c + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#if DDIT_FMHA_PTMEM
+        tmem_st_wait();
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 31) mbar_arrive(&p_full[g]);  // release (P stores), from a lane without bulk copies
