@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import torch
@@ -142,6 +143,7 @@ class B200Executor:
         self.nvlink_gbs = nvlink_gbs
         self.pool: dict[tuple, list[_Live]] = {}  # (resolution, devices) -> idle groups
         self.pool_limit = 4
+        self._enqueue_pool: ThreadPoolExecutor | None = None  # per-rank step enqueue threads
         self.reshard_host_seconds: list[float] = []  # promotion wall time, device wait included
         self.reshard_enqueue_seconds: list[float] = []  # host work to enqueue the re-shard
         # when set, every request's denoised latent (+ frames with keep_videos) is also written
@@ -380,14 +382,23 @@ class B200Executor:
                 e.record()
                 e.synchronize()
                 return s.elapsed_time(e) / 1e3
-        evs = []
-        for r, zs in zip(live.ranks, live.shards):
+        # one host thread per rank enqueues that rank's step on its own device (the C calls drop
+        # the GIL): a rank whose kernels wait on peer flags never depends on the host having
+        # already queued the peers' ~600 launches behind it
+        def run(i: int):
+            r, zs = live.ranks[i], live.shards[i]
             with torch.cuda.device(zs.device):
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
                 r.step(zs, step)
                 e.record()
-                evs.append((s, e))
+                return s, e
+        if len(live.ranks) == 1:
+            evs = [run(0)]
+        else:
+            if self._enqueue_pool is None or self._enqueue_pool._max_workers < len(live.ranks):
+                self._enqueue_pool = ThreadPoolExecutor(max_workers=max(8, len(live.ranks)))
+            evs = list(self._enqueue_pool.map(run, range(len(live.ranks))))
         for _, e in evs:
             e.synchronize()
         return max(s.elapsed_time(e) for s, e in evs) / 1e3
@@ -402,6 +413,9 @@ class B200Executor:
             r.close()
 
     def close(self) -> None:
+        if self._enqueue_pool is not None:
+            self._enqueue_pool.shutdown()
+            self._enqueue_pool = None
         for idle in self.pool.values():
             for live in idle:
                 for r in live.ranks:
