@@ -50,6 +50,9 @@ DDIT_API int ddit_set_fused_exchange(int on);
  * through a TMA reduce-add into the fp32 residual (no residual loads), 0 = TMA load / update /
  * store. Both give bit-identical results. Env DDIT_RESID_RED=0; applies to plans built afterwards. */
 DDIT_API int ddit_set_resid_reduce(int on);
+/* 2-CTA GEMMs with K >= 4096 and BN 192 (fc2) as 256 x 384 tiles -- two accumulator halves, one
+ * tile in TMEM -- (default 1; env DDIT_GEMM_WIDE=0); bit-identical results. Plans built afterwards. */
+DDIT_API int ddit_set_gemm_wide(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */

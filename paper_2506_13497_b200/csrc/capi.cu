@@ -107,6 +107,10 @@ DDIT_API int ddit_set_gemm_2cta(int on) {
   set_two_cta(on);
   return DDIT_OK;
 }
+DDIT_API int ddit_set_gemm_wide(int on) {
+  set_gemm_wide(on);
+  return DDIT_OK;
+}
 
 DDIT_API int ddit_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int epi,
                        const ddit_epi* ep, int bn, void* stream) {

@@ -222,6 +222,19 @@ DDIT_DEV void resid_prefetch_l2(const ResidStream& rs, int i, const CUtensorMap*
                  : "memory");
 }
 
+// the same for a wide tile (2BN columns): both BN halves
+template <int BN>
+DDIT_DEV void resid_prefetch_l2_wide(const ResidStream& rs, int i, const CUtensorMap* tmP) {
+  int m0, c0;
+  if (rs.coord(i * (2 * BN / 32), 2 * BN / 32, m0, c0))
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                       reinterpret_cast<uint64_t>(tmP)),
+                   "r"(c0 + h * BN), "r"(m0)
+                   : "memory");
+}
+
 // load residual sub-tile j of this warp's 32-row slab into ring slot j % R (wbase: the warp's
 // ring, wbar: its R barriers)
 template <int R>
@@ -842,10 +855,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // [128r, 128r+128) of A and rows [r*BN/2, (r+1)*BN/2) of B in its smem and the accumulator rows
 // [128r, 128r+128) x BN in its TMEM; the leader (rank 0) issues tcgen05.mma.cta_group::2 with
 // M = 256. Each SM streams half the B operand of the 1-CTA kernel.
-template <int BN, int EPI>
+template <int BN, int EPI, int WIDE = 1>
 struct GemmCfg2 {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int B_BYTES = WIDE * (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 512;
   static constexpr int BUDGET = 232448 - 1024 - BAR_BYTES - EpiCfg<BN, EPI>::BYTES;
@@ -881,7 +894,11 @@ DDIT_DEV void umma_commit_cg2_mc(uint64_t* bar) {  // arrive on `bar` in both CT
       : "memory");
 }
 
-template <int BN, int EPI>
+// WIDE = 2: each tile is 256 x 2BN, computed as two N = BN MMAs per k-step into the two TMEM
+// accumulator halves [0, BN) and [BN, 2BN) (one tile in flight, no double buffer): per k-block the
+// A stage is written once for 2BN output columns, which lowers the shared-memory traffic per
+// FLOP; the epilogue drains half 0 then half 1, each with the BN epilogue.
+template <int BN, int EPI, int WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
@@ -889,9 +906,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tmR,
                          const __grid_constant__ CUtensorMap tmO2, int M, int N, int K,
                          const __grid_constant__ EpiParams ep) {
-  using Cfg = GemmCfg2<BN, EPI>;
+  using Cfg = GemmCfg2<BN, EPI, WIDE>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int BM2 = 2 * BM;
+  constexpr int TW = WIDE * BN;  // output columns per tile
+  static_assert(WIDE == 1 || TW <= 512, "wide tile exceeds TMEM");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -913,7 +932,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cx.M = M;
   cx.N = N;
   cx.m_tiles = (M + BM2 - 1) / BM2;
-  cx.n_tiles = N / BN;
+  cx.n_tiles = N / TW;
   cx.num_tiles = cx.m_tiles * cx.n_tiles;
   const int n_tiles = cx.n_tiles;
   const int num_tiles = cx.num_tiles;
@@ -957,13 +976,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = cid; tile < num_tiles; tile += nclusters) {
         const int m0 = (tile / n_tiles) * BM2 + rank * BM;
-        const int nb0 = (tile % n_tiles) * BN + rank * (BN / 2);
+        const int nb0 = (tile % n_tiles) * TW + rank * (BN / 2);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
           const uint32_t bar0 = cluster_addr(&full[stage], 0);
           tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, bar0, kb * BK, m0, pol_a);
-          tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, bar0, kb * BK, nb0, pol_b);
+#pragma unroll
+          for (int h = 0; h < WIDE; ++h)  // half h: output columns [h BN, h BN + BN) of the tile
+            tma_load_2d_cg2(sB + stage * Cfg::B_BYTES + h * (BN / 2) * BK * 2, &tmB, bar0, kb * BK,
+                            nb0 + h * BN, pol_b);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -983,9 +1005,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int tile = cid; tile < num_tiles; tile += nclusters, ++tt) {
         if (lane == 0) EPI_TRACE(2 * tt);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if constexpr (WIDE == 2) mbar_wait(&tempty[1], acc_phase ^ 1);  // both halves drained
         tc_fence_after();
         if (lane == 0) EPI_TRACE(2 * tt + 1);
-        const uint32_t d_tmem = tmem_base + acc * kAccStride;
+        const uint32_t d_tmem = tmem_base + (WIDE == 2 ? 0u : acc * kAccStride);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -996,10 +1019,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_ss_cg2(d_tmem, make_sdesc_sw128(a_base + k * 32),
-                               make_sdesc_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+#pragma unroll
+              for (int h = 0; h < WIDE; ++h)
+                umma_bf16_ss_cg2(d_tmem + h * BN, make_sdesc_sw128(a_base + k * 32),
+                                 make_sdesc_sw128(b_base + h * (BN / 2) * BK * 2 + k * 32), idesc,
+                                 (kb | k) != 0);
             umma_commit_cg2_mc(&empty[stage]);
-            if (kb == k_blocks - 1) umma_commit_cg2_mc(&tfull[acc]);
+            if (kb == k_blocks - 1) {
+              umma_commit_cg2_mc(&tfull[acc]);
+              if constexpr (WIDE == 2) umma_commit_cg2_mc(&tfull[1]);
+            }
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -1007,8 +1036,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if constexpr (WIDE == 2) {
+          acc_phase ^= 1;
+        } else {
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {  // ---- epilogue (both CTAs): own 128 accumulator rows
@@ -1038,28 +1071,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int tix = 0;
     for (int tile = cid; tile < num_tiles; tile += nclusters) {
       const int m0 = (tile / n_tiles) * BM2 + rank * BM;
-      const int n0 = (tile % n_tiles) * BN;
+      const int nt0 = (tile % n_tiles) * TW;
       if constexpr (is_resid(EPI)) {  // two tiles ahead: lands in L2 well before its epilogue
-        if (elected) resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
+        if (elected) {
+          if constexpr (WIDE == 2) {
+            resid_prefetch_l2_wide<BN>(rs, tix + 2, &tmO);
+          } else {
+            resid_prefetch_l2<BN>(rs, tix + 2, &tmO);
+          }
+        }
         ++tix;
       }
-      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1));
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1) + 1);
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
-      const uint32_t tcl = cluster_addr(&tempty[acc], 0);
-      if constexpr (EPI == EPI_QKV) {
-        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
-      } else if constexpr (EPI == EPI_RESID_RED) {
-        epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
-      } else if constexpr (is_resid(EPI)) {
-        epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
-      } else {
-        epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+#pragma unroll 1
+      for (int h = 0; h < WIDE; ++h) {
+        const int hb = WIDE == 2 ? h : acc;  // accumulator half / buffer
+        const int n0 = nt0 + h * BN;
+        if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1));
+        mbar_wait(&tfull[hb], acc_phase);
+        tc_fence_after();
+        if (ew == 0 && lane == 0) EPI_TRACE(128 + 2 * (tix - 1) + 1);
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                               (WIDE == 2 ? hb * BN : hb * kAccStride);
+        const uint32_t tcl = cluster_addr(&tempty[hb], 0);
+        if constexpr (EPI == EPI_QKV) {
+          epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+        } else if constexpr (EPI == EPI_RESID_RED) {
+          epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
+        } else if constexpr (is_resid(EPI)) {
+          epi_resid_tile<BN, EPI>(ep, &tmR, &tmO2, sE, rbar, taddr, ew, lane, m0, n0, cx, rs, cnt, tcl, sCol);
+        } else {
+          epi_plain_tile<BN, EPI>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+        }
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if constexpr (WIDE == 2) {
+        acc_phase ^= 1;
+      } else {
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
     }
     if (elected || ((is_resid(EPI) || EPI == EPI_QKV) && lane == 0)) bulk_wait<0>();
   }
@@ -1254,8 +1303,12 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
   p->bn = bn;
   p->epi = epi;
   p->ep = ep;
+  // 256 x 384 tiles only where the long K loop hides the un-overlapped epilogue (fc2, K = 4608:
+  // 94.0 -> 91.3 us; at K = 1152 they lose 13-16 %, scripts/wide_probe.py); bit-identical results
+  p->wide = p->two_cta && bn == 192 && N % (2 * bn) == 0 && K >= 4096 && gemm_wide_enabled() &&
+            (epi == EPI_RESID_RED || epi == EPI_BF16) && !ep.xch;
   if (p->two_cta) {
-    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / bn);
+    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / (bn * (p->wide ? 2 : 1)));
     const int clusters = num_sms() / 2;
     p->grid = 2 * (tiles < clusters ? tiles : clusters);
   } else {
@@ -1285,6 +1338,16 @@ bool pdl_enabled() {
 }
 void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
+static int g_wide = -1;
+bool gemm_wide_enabled() {
+  if (g_wide < 0) {
+    const char* e = getenv("DDIT_GEMM_WIDE");
+    g_wide = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_wide != 0;
+}
+void set_gemm_wide(int on) { g_wide = on ? 1 : 0; }
+
 static int g_two_cta = -1;
 bool two_cta_enabled() {
   if (g_two_cta < 0) {
@@ -1295,18 +1358,18 @@ bool two_cta_enabled() {
 }
 void set_two_cta(int on) { g_two_cta = on ? 1 : 0; }
 
-template <int BN, int EPI>
-static int launch_t2(const GemmPlan* p, cudaStream_t s) {
-  constexpr int smem = GemmCfg2<BN, EPI>::SMEM;
+template <int BN, int EPI, int WIDE>
+static int launch_t2w(const GemmPlan* p, cudaStream_t s) {
+  constexpr int smem = GemmCfg2<BN, EPI, WIDE>::SMEM;
   static size_t attr[64] = {};
   {
-    cudaError_t e = ensure_smem((const void*)gemm2_bf16_tn_kernel<BN, EPI>, smem, attr);
+    cudaError_t e = ensure_smem((const void*)gemm2_bf16_tn_kernel<BN, EPI, WIDE>, smem, attr);
     if (e != cudaSuccess) {
       snprintf(g_err, sizeof g_err, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
       return -4;
     }
   }
-  launch_pdl(gemm2_bf16_tn_kernel<BN, EPI>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
+  launch_pdl(gemm2_bf16_tn_kernel<BN, EPI, WIDE>, dim3(p->grid), dim3(kThreads), smem, s, p->tmA, p->tmB,
              p->tmO, p->tmR, p->tmO2, p->M, p->N, p->K, p->ep);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -1314,6 +1377,13 @@ static int launch_t2(const GemmPlan* p, cudaStream_t s) {
     return -4;
   }
   return 0;
+}
+
+template <int BN, int EPI>
+static int launch_t2(const GemmPlan* p, cudaStream_t s) {
+  if constexpr (BN == 192 && (EPI == EPI_RESID_RED || EPI == EPI_BF16))
+    if (p->wide) return launch_t2w<BN, EPI, 2>(p, s);
+  return launch_t2w<BN, EPI, 1>(p, s);
 }
 
 template <int BN, int EPI>

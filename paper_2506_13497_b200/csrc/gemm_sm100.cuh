@@ -65,6 +65,7 @@ struct GemmPlan {
   EpiParams ep;
   int grid;
   int two_cta;  // 1: cta_group::2 kernel (M = 256 tiles over a CTA pair)
+  int wide;     // 1: 2-CTA tiles of 256 x 2BN (two accumulator halves, one tile in TMEM)
 };
 
 // Build the TMA descriptors and launch geometry. Returns 0 on success.
@@ -77,6 +78,8 @@ void gemm_pick_tile(int M, int N, int epi, int* bn, int* two_cta);
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
 int num_sms();
 bool two_cta_enabled();
+bool gemm_wide_enabled();
+void set_gemm_wide(int on);
 bool resid_red_enabled();
 void set_resid_red(int on);
 void set_pdl(int on);

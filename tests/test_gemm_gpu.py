@@ -155,3 +155,39 @@ def test_gemm_resid_gate_many_batches(cuda, nb, N):
     kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate, rows_per_b=rows_per_b, bn=192)
     b = torch.arange(M, device=cuda) // rows_per_b
     assert rel_l2(x, x0 + gate[b] * (a.float() @ w.float().T + bias)) < 1e-5
+
+
+@pytest.mark.parametrize("M", [12150, 1000, 300])
+@pytest.mark.parametrize("red", [True, False], ids=["reduce-add", "bf16"])
+def test_gemm_wide_tiles_bit_identical(cuda, gemm_mode, M, red):
+    """The 256 x 384 tiles (two BN = 192 accumulator halves, fc2's K = 4608) reproduce the
+    256 x 192 tiles bit for bit, with the reduce-add residual and the plain bf16 epilogue; the
+    1-CTA parametrisation runs the regular kernel on both sides."""
+    from paper_2506_13497_b200 import _lib, kernels
+
+    N, K = 1152, 4608
+    a, w, bias = _inputs(M, N, K, cuda, seed=7)
+    gate = torch.randn(2, N, device=cuda)
+    x0 = torch.randn(M, N, device=cuda)
+    outs = []
+    for wide in (1, 0):
+        _lib.lib().ddit_set_gemm_wide(wide)
+        try:
+            if red:
+                x = x0.clone()
+                kernels.gemm(a, w, epi=_lib.EPI_RESID, bias=bias, resid=x, gate=gate,
+                             rows_per_b=(M + 1) // 2, bn=192)
+                outs.append(x)
+            else:
+                out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+                kernels.gemm(a, w, epi=_lib.EPI_BF16, bias=bias, out=out, bn=192)
+                outs.append(out)
+        finally:
+            _lib.lib().ddit_set_gemm_wide(1)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = a.float() @ w.float().T + bias
+    if red:
+        b = torch.arange(M, device=cuda) // ((M + 1) // 2)
+        ref = x0 + gate[b] * ref
+    assert rel_l2(outs[0], ref) < 1e-2
