@@ -53,6 +53,9 @@ DDIT_API int ddit_set_resid_reduce(int on);
 /* 2-CTA GEMMs with K >= 4096 and BN 192 (fc2) as 256 x 384 tiles -- two accumulator halves, one
  * tile in TMEM -- (default 1; env DDIT_GEMM_WIDE=0); bit-identical results. Plans built afterwards. */
 DDIT_API int ddit_set_gemm_wide(int on);
+/* QKV GEMM on per-head padded weights (80-row head slots, 256 x 240 tiles; default 1; env
+ * DDIT_QKV_PAD=0); bit-identical results. Applies to requests opened afterwards. */
+DDIT_API int ddit_set_qkv_pad(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */

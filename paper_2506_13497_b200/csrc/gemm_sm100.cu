@@ -56,7 +56,8 @@ struct EpiCfg {
   // staging bytes (two buffers) and sub-tile width (columns) per epilogue kind: bf16 outputs
   // use 64-column sub-tiles (128 B swizzle) when BN allows, else 32 (64 B swizzle)
   static constexpr bool BF = EPI == EPI_BF16 || EPI == EPI_GELU_BF16;
-  static constexpr int SUB = EPI == EPI_QKV ? 72 : BF ? (BN % 64 == 0 ? 64 : 32) : 32;
+  // QKV: one head per sub-tile, in 72-column slots (BN 144) or 80-column padded slots (BN 240)
+  static constexpr int SUB = EPI == EPI_QKV ? (BN == 240 ? 80 : 72) : BF ? (BN % 64 == 0 ? 64 : 32) : 32;
   static constexpr int BUF = EPI == EPI_QKV ? 128 * 144 : 128 * 128;  // main staging buffer
   // gated residual: each epilogue warp runs its own ring of RSLOTS fp32 32x32 sub-tiles (loads run
   // RSLOTS-2 sub-tiles ahead) + three bf16 copy buffers (SW64): WARP_BYTES per warp
@@ -81,7 +82,7 @@ struct EpiCfg {
   // QKV: bias. Plain epilogues keep __ldg: staging their bias cost 1.3 ms per 144p step (small-M
   // GEMMs have one or two tiles per CTA, so the per-CTA staging is not amortised)
   // sized to the XL/2 need (3 x 1152 or 3456 floats = 13.5 KB), so QKV keeps 7 mainloop stages
-  static constexpr int COL_BYTES = is_resid(EPI) || EPI == EPI_QKV ? 13824 : 0;
+  static constexpr int COL_BYTES = is_resid(EPI) ? 13824 : EPI == EPI_QKV ? (BN == 240 ? 15360 : 13824) : 0;
   static constexpr int BYTES = is_resid(EPI) ? 4 * WARP_BYTES + COL_BYTES : 2 * BUF + COL_BYTES;
 };
 static constexpr int kRBars = 4 * 5;  // residual ring barriers (per warp) in the barrier block
@@ -594,33 +595,40 @@ DDIT_DEV void epi_red_tile(const EpiParams& ep, const CUtensorMap* tmR, uint8_t*
 // ------------------------------------------------------------------ epilogue: QKV
 // The 144-column tile holds two whole heads (head_dim 72) of one of q/k/v.
 // q,k: bias -> per-head RMSNorm (weight) -> optional interleaved RoPE by frame index.
+// NH heads per tile in HS-column slots: HS = 72 (the QKV matrix as is, BN 144) or HS = 80 (the
+// weight rows padded per head with 8 zero rows, BN 240 = 3 heads: the shared-memory-cheaper
+// tile shape, §3 of DESIGN.md); the output always has 72-column head slots. The padded columns
+// are computed (zero) and dropped.
+template <int NH, int HS>
 DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t* sE,
                            uint32_t taddr, int rit, int m0, int n0, bool elected, int& cnt,
                            uint32_t tempty_cl, int lane, const float* sCol) {
   constexpr int HD = 72;
-  const int section = n0 / ep.hidden;  // 0 q, 1 k, 2 v
+  const int heads = ep.hidden / HD;
   const int row = m0 + rit;
   const int pos = ep.rope ? (row / ep.rope_S) % ep.rope_T : 0;
   // per-warp staging (32 rows x 144 B, double-buffered) and per-warp TMA stores: the four
   // epilogue warps never wait for each other
   const int ew = rit >> 5;
 #pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NH; ++h) {
+    const int hi = n0 / HS + h;        // head slot in [0, 3 heads)
+    const int section = hi / heads;    // 0 q, 1 k, 2 v
     uint8_t* sb = sE + ew * 9216 + (cnt & 1) * 4608;
     const uint32_t sbase = smem_u32(sb) + lane * 144;
     if (lane == 0) bulk_wait_read<1>();  // this warp's store of two heads ago has read sb
     __syncwarp();
     uint32_t r[72];
-    tmem_ld_x32(taddr + h * HD, r);
-    tmem_ld_x32(taddr + h * HD + 32, r + 32);
-    tmem_ld_32x32b_x8(taddr + h * HD + 64, r + 64);
+    tmem_ld_x32(taddr + h * HS, r);
+    tmem_ld_x32(taddr + h * HS + 32, r + 32);
+    tmem_ld_32x32b_x8(taddr + h * HS + 64, r + 64);
     tmem_ld_wait();
-    if (h == 1) {
+    if (h == NH - 1) {
       tc_fence_before();
       __syncwarp();
       if (lane == 31) mbar_arrive_cl_relaxed(tempty_cl);
     }
-    const int c0 = n0 + h * HD;
+    const int c0 = n0 + h * HS;  // bias column (same slot layout as the GEMM's N)
     float v[72];
     float ss = 0.f;
 #pragma unroll
@@ -666,7 +674,7 @@ DDIT_DEV void epi_qkv_tile(const EpiParams& ep, const CUtensorMap* tmO, uint8_t*
     fence_async_smem();
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(tmO, sb, c0, m0 + ew * 32);
+      tma_store_2d(tmO, sb, hi * HD, m0 + ew * 32);
       bulk_commit();
     }
     ++cnt;
@@ -826,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kAccStride;
       const uint32_t tcl = cluster_addr(&tempty[acc], 0);
       if constexpr (EPI == EPI_QKV) {
-        epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+        epi_qkv_tile<BN == 240 ? 3 : 2, BN == 240 ? 80 : 72>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
       } else if constexpr (EPI == EPI_RESID_RED) {
         epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
       } else if constexpr (is_resid(EPI)) {
@@ -1094,7 +1102,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                (WIDE == 2 ? hb * BN : hb * kAccStride);
         const uint32_t tcl = cluster_addr(&tempty[hb], 0);
         if constexpr (EPI == EPI_QKV) {
-          epi_qkv_tile(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
+          epi_qkv_tile<BN == 240 ? 3 : 2, BN == 240 ? 80 : 72>(ep, &tmO, sE, taddr, rit, m0, n0, elected, cnt, tcl, lane, sCol);
         } else if constexpr (EPI == EPI_RESID_RED) {
           epi_red_tile<BN>(ep, &tmR, sE, taddr, ew, lane, m0, n0, cx, cnt, tcl, sCol);
         } else if constexpr (is_resid(EPI)) {
@@ -1186,7 +1194,7 @@ int num_sms() {
 }
 
 static bool bn_ok(int bn, int epi) {
-  if (epi == EPI_QKV) return bn == 144;
+  if (epi == EPI_QKV) return bn == 144 || bn == 240;
   if (epi == EPI_RESID_COPY) return bn == 128 || bn == 192 || bn == 256;
   if (bn == 0) return false;
   return bn == 96 || bn == 128 || bn == 192 || bn == 256;
@@ -1235,8 +1243,8 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
     snprintf(g_err, sizeof g_err, "bad GEMM shape M=%d N=%d K=%d BN=%d", M, N, K, bn);
     return -2;
   }
-  if (epi == EPI_QKV && ep.hidden % 144 != 0) {
-    snprintf(g_err, sizeof g_err, "EPI_QKV needs hidden %% 144 == 0");
+  if (epi == EPI_QKV && (ep.hidden % 144 != 0 || N != (bn == 240 ? 3 * ep.hidden / 72 * 80 : 3 * ep.hidden))) {
+    snprintf(g_err, sizeof g_err, "EPI_QKV needs hidden %% 144 == 0 and N = 3 heads x (72 | 80 at BN 240)");
     return -2;
   }
   if ((lda * 2) % 16 || (ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
@@ -1264,8 +1272,8 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
       if (!ep.out || make_tmap(&p->tmO, ep.out, F32, 4, M, N, ep.ldo, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return -3;
       break;
-    case EPI_QKV:
-      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, N, ep.ldo, 32, 72, CU_TENSOR_MAP_SWIZZLE_NONE))
+    case EPI_QKV:  // output: 72-column head slots whatever the GEMM's slot width
+      if (!ep.out || make_tmap(&p->tmO, ep.out, BF, 2, M, 3 * ep.hidden, ep.ldo, 32, 72, CU_TENSOR_MAP_SWIZZLE_NONE))
         return -3;
       break;
     case EPI_RESID:
@@ -1413,7 +1421,7 @@ int gemm_plan_launch(const GemmPlan* p, cudaStream_t s) {
   // on the fc2 plans) needs the load / update / store epilogue: its rows go to their owners
   const int epi = p->epi == EPI_RESID_RED && (p->ep.xch || p->ep.out2) ? EPI_RESID : p->epi;
   switch (epi) {
-    case EPI_QKV: return launch_t<144, EPI_QKV>(p, s);
+    case EPI_QKV: return p->bn == 240 ? launch_t<240, EPI_QKV>(p, s) : launch_t<144, EPI_QKV>(p, s);
     case EPI_BF16:
       switch (p->bn) {
         case 96: return launch_t<96, EPI_BF16>(p, s);

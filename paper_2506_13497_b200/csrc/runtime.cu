@@ -43,10 +43,39 @@ struct ddit_model {
   // so a request's whole K/V cache is ONE GEMM (M = B*300, N = 2*depth*2C = 129024 at XL/2)
   bf16* ckv_all = nullptr;
   float* ckv_b_all = nullptr;
+  // every block's QKV weight with each head's 72 rows padded to an 80-row slot (8 zero rows) and
+  // the bias likewise: the QKV GEMM then runs 256 x 240 tiles (3 whole heads, the per-head
+  // RMSNorm / RoPE epilogue intact) instead of 256 x 144 -- shared-memory traffic per FLOP 178 ->
+  // 131 B/clk; the padded columns are zeros and never stored
+  bf16* qkv_pad = nullptr;
+  float* qkv_bpad = nullptr;
 };
 
 namespace {
 enum { G_QKV = 0, G_PROJ, G_CQ, G_CPROJ, G_FC1, G_FC2, G_N };
+
+constexpr int kQkvSlot = 80;  // padded head slot of the QKV GEMM (rows of qkv_pad per head)
+
+// dst row r of a [3 heads x 80] padded matrix <- src row (r / 80) * 72 + r % 80, zero if r % 80 >= 72
+__global__ void qkv_pad_kernel(const bf16* __restrict__ w, const float* __restrict__ b,
+                               bf16* __restrict__ wp, float* __restrict__ bp, int rows_pad, int C) {
+  const int r = blockIdx.x;
+  const int slot = r / kQkvSlot, j = r % kQkvSlot;
+  const bool real = j < 72;
+  const uint4* src = reinterpret_cast<const uint4*>(w + (size_t)(slot * 72 + (real ? j : 0)) * C);
+  uint4* dst = reinterpret_cast<uint4*>(wp + (size_t)r * C);
+  for (int i = threadIdx.x; i < C / 8; i += blockDim.x) dst[i] = real ? src[i] : make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) bp[r] = real ? b[slot * 72 + j] : 0.f;
+}
+
+int g_qkv_pad = -1;  // DDIT_QKV_PAD=0: the unpadded 144-column tiles
+bool qkv_pad_enabled() {
+  if (g_qkv_pad < 0) {
+    const char* e = getenv("DDIT_QKV_PAD");
+    g_qkv_pad = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_qkv_pad != 0;
+}
 
 struct Geometry {
   int B = 2;
@@ -283,8 +312,15 @@ int build_plans(ddit_req* r) {
     e.rope_tab = reinterpret_cast<const float2*>(r->rope);
     e.eps = c.eps;
     e.rows_per_b = rpb;
-    if ((rc = plan_auto(&P[G_QKV], r->xm, C, bw.qkv_w, C, M, 3 * C, C, EPI_QKV, e)))
+    if (r->m->qkv_pad && qkv_pad_enabled()) {
+      const int rows_pad = 3 * c.heads * kQkvSlot;
+      e.bias = r->m->qkv_bpad + (size_t)k * rows_pad;
+      if ((rc = gemm_plan_init_cta(&P[G_QKV], r->xm, C, r->m->qkv_pad + (size_t)k * rows_pad * C, C, M,
+                                   rows_pad, C, EPI_QKV, e, 240, two_cta_enabled() ? 1 : 0)))
+        return rc;
+    } else if ((rc = plan_auto(&P[G_QKV], r->xm, C, bw.qkv_w, C, M, 3 * C, C, EPI_QKV, e))) {
       return rc;
+    }
     // attention out-projection: x += gate_msa * (.) ; bf16 copy of x for cross-attn queries
     memset(&e, 0, sizeof e);
     e.bias = bw.proj_b;
@@ -584,7 +620,26 @@ DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, dd
     ddit_model_destroy(m);
     return DDIT_E_ALLOC;
   }
+  const int rows_pad = 3 * cfg->heads * kQkvSlot;
+  ok = cudaMalloc(&m->qkv_pad, (size_t)2 * cfg->depth * rows_pad * cfg->hidden * sizeof(bf16)) == cudaSuccess &&
+       cudaMalloc(&m->qkv_bpad, (size_t)2 * cfg->depth * rows_pad * sizeof(float)) == cudaSuccess;
+  for (int k = 0; ok && k < 2 * cfg->depth; ++k) {
+    qkv_pad_kernel<<<rows_pad, 128>>>(static_cast<const bf16*>(m->blocks[k].qkv_w), m->blocks[k].qkv_b,
+                                      m->qkv_pad + (size_t)k * rows_pad * cfg->hidden,
+                                      m->qkv_bpad + (size_t)k * rows_pad, rows_pad, cfg->hidden);
+    ok = cudaGetLastError() == cudaSuccess;
+  }
+  if (!ok || cudaDeviceSynchronize() != cudaSuccess) {
+    set_error("ddit_model_create: padded QKV weights: %s", cudaGetErrorString(cudaGetLastError()));
+    ddit_model_destroy(m);
+    return DDIT_E_ALLOC;
+  }
   *out = m;
+  return DDIT_OK;
+}
+
+DDIT_API int ddit_set_qkv_pad(int on) {
+  g_qkv_pad = on ? 1 : 0;
   return DDIT_OK;
 }
 
@@ -593,6 +648,8 @@ DDIT_API void ddit_model_destroy(ddit_model* m) {
   cudaFree(m->sst_dev);
   cudaFree(m->ckv_all);
   cudaFree(m->ckv_b_all);
+  cudaFree(m->qkv_pad);
+  cudaFree(m->qkv_bpad);
   delete m;
 }
 

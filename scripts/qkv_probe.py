@@ -50,3 +50,13 @@ for rope in (False, True):
                                    rope_tab=tab if rope else None, rope_T=15, rope_S=405, bn=144,
                                    stream=torch.cuda.current_stream()))
     print(f"qkv epilogue bn=144 rope={rope}: {t*1e3:7.1f} us {fl/t/1e9:7.1f} TF/s", flush=True)
+# per-head padded weights (80-row slots): the 256 x 240 tile
+wp = torch.zeros(48 * 80, K, device=dev, dtype=torch.bfloat16)
+bp = torch.zeros(48 * 80, device=dev)
+for h in range(48):
+    wp[h * 80:h * 80 + 72] = w[h * 72:(h + 1) * 72]
+for rope in (False, True):
+    t = gtime(lambda: kernels.gemm(a, wp, epi=_lib.EPI_QKV, bias=bp, out=out, qnorm_w=qw, knorm_w=qw, hidden=1152,
+                                   rope_tab=tab if rope else None, rope_T=15, rope_S=405, bn=240,
+                                   stream=torch.cuda.current_stream()))
+    print(f"qkv epilogue padded bn=240 rope={rope}: {t*1e3:7.1f} us {fl/t/1e9:7.1f} TF/s (algorithmic)", flush=True)

@@ -298,3 +298,30 @@ def test_exchange_barrier_times_out_instead_of_hanging(cuda):
             r0.status()
     finally:
         lib.ddit_set_exchange_timeout_ms(0)
+
+
+@pytest.mark.parametrize("cfg_name,label", [("TINY", "144p-16f"), ("XL2", "240p")])
+def test_padded_qkv_tiles_bit_identical(cuda, cfg_name, label):
+    """The QKV GEMM on per-head padded weights (256 x 240 tiles, 80-column head slots) gives the
+    same step bit for bit as the unpadded 256 x 144 tiles (XL/2 width at depth 1; tiny: 4 heads)."""
+    from paper_2506_13497_b200 import _lib, weights
+    from paper_2506_13497_b200.stdit import STDiTModel, StepRequest
+
+    cfg = getattr(weights, cfg_name)
+    if cfg_name == "XL2":
+        cfg = dataclasses.replace(cfg, depth=1)
+    W, sh, z, y = _setup(cfg, label)
+    model = STDiTModel(cfg, W, cuda)
+    outs = []
+    for pad in (1, 0):
+        _lib.lib().ddit_set_qkv_pad(pad)
+        try:
+            req = StepRequest(model, sh, y.to(cuda))
+        finally:
+            _lib.lib().ddit_set_qkv_pad(1)
+        zd = z.to(cuda).contiguous()
+        req.step(zd, 4)
+        torch.cuda.synchronize()
+        outs.append(zd.cpu())
+        req.close()
+    assert torch.equal(outs[0], outs[1])
