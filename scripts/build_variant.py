@@ -16,6 +16,8 @@ out_dir.mkdir(parents=True, exist_ok=True)
 obj = out_dir / (Path(src).stem + ".o")
 src_path = Path(src) if Path(src).is_absolute() else b.CSRC / src  # absolute: e.g. an older revision
 subprocess.run([b.NVCC, *b.ARCH, *b.FLAGS, *extra, "-c", str(src_path), "-o", str(obj)], check=True)
+if obj.stem not in {s.stem for s in b._sources()}:
+    sys.exit(f"{src}: the variant source must keep the name of the csrc file it replaces")
 objs = [obj if o.stem == obj.stem else o for o in (b.BUILD / (s.stem + ".o") for s in b._sources())]
 lib = b.PKG / f"libddit_{name}.so"
 subprocess.run([b.NVCC, *b.ARCH, "-shared", "-o", str(lib), *map(str, objs), "-cudart", "shared",
