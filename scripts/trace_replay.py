@@ -65,7 +65,7 @@ def main() -> None:
         for d in (1, 2, 4, 8):
             req = RequestState(90_000 + len(entries), res, 0.0, a.steps)
             ex.dit_step(req, tuple(range(d)), 0, None)  # open + warm-up
-            times = [ex._run_step(ex.live[req.request_id], 1 + i) for i in range(3)]
+            times = [ex._run_step(ex.live[req.request_id], 1 + i) for i in range(5)]
             ex._close(ex.live.pop(req.request_id))
             e = {"resolution": res, "dop": d, "dit_step_seconds": round(min(times), 6)}
             if d == 1:
