@@ -56,6 +56,9 @@ DDIT_API int ddit_set_gemm_wide(int on);
 /* QKV GEMM on per-head padded weights (80-row head slots, 256 x 240 tiles; default 1; env
  * DDIT_QKV_PAD=0); bit-identical results. Applies to requests opened afterwards. */
 DDIT_API int ddit_set_qkv_pad(int on);
+/* VAE convolutions as cta_group::2 pairs of 128-pixel tiles (half the weight rows per CTA) when
+ * there are enough tiles (default 1; env DDIT_CONV_2CTA=0); bit-identical results. */
+DDIT_API int ddit_set_conv_2cta(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */

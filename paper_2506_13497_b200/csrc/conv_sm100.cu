@@ -10,7 +10,14 @@
 // buffered), warp-specialised pipeline as in gemm_sm100.cu; the epilogue adds the bias and an
 // optional bf16 residual (TMA-loaded, prefetched one sub-tile ahead) and leaves through
 // swizzled smem + TMA stores clipped at the frame edges.
+//
+// conv2_kernel: the same as a cta_group::2 pair (one TPC): CTA r of the cluster takes pixel tile
+// 2 q + r of channel block n, holds half of the BN weight rows, and the leader issues M = 256
+// MMAs. Per CTA and k-block the shared memory then sees A (16 KB) + B / 2 written and read instead
+// of A + B: at BN = 256 that is 125 instead of 187 B/clk of the 128 B/clk the SM's shared memory
+// moves, the bound the 1-CTA kernel sat at.
 #include "common.cuh"
+#include "cta_pair.cuh"
 #include "ddit.h"
 #include "capi_internal.h"
 
@@ -35,12 +42,26 @@ struct Cfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR;
 };
 
+template <int BN, bool RES>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int EPI = 2 * 16384;
+  static constexpr int BAR = 256;
+  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - EPI) / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR;
+  static_assert(B_BYTES % 1024 == 0, "B half-tile must keep 1024 B swizzle-atom alignment");
+};
+
 struct Params {
   int B, T, H, W, Cin, Cout;
   int kt, kh, kw, pt, ph, pw;
   int Wt, R, x_tiles, y_tiles, n_tiles, num_tiles;
   int cblocks, k_blocks;
   int a_bytes;
+  int pix_tiles, pair_tiles;  // 2-CTA: pixel tiles, and (pixel-tile pair, channel block) tiles
   const float* bias;
 };
 
@@ -104,6 +125,231 @@ DDIT_DEV TileCoord decode(const Params& p, int tile, int BN) {
   c.x0 = xt * p.Wt;
   c.n0 = nt * BN;
   return c;
+}
+
+// pair tile pt, CTA rank r -> pixel tile 2 (pt / n_tiles) + r, channel block pt % n_tiles. A rank
+// without a pixel tile (odd count) gets the last tile moved past the right edge: its loads are all
+// zero fill and it stores nothing (returns false).
+DDIT_DEV bool decode2(const Params& p, int pt, int rank, int BN, TileCoord& c) {
+  const int nt = pt % p.n_tiles;
+  const int pix2 = 2 * (pt / p.n_tiles) + rank;
+  const bool real = pix2 < p.pix_tiles;
+  int pix = real ? pix2 : p.pix_tiles - 1;
+  const int xt = pix % p.x_tiles;
+  pix /= p.x_tiles;
+  const int yt = pix % p.y_tiles;
+  pix /= p.y_tiles;
+  c.t = pix % p.T;
+  c.b = pix / p.T;
+  c.y0 = yt * p.R;
+  c.x0 = real ? xt * p.Wt : p.W;
+  c.n0 = nt * BN;
+  return real;
+}
+
+template <int BN, bool RES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    conv2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                 const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmR,
+                 const __grid_constant__ Params p) {
+  using C = Cfg2<BN, RES>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint8_t* sE = smem + STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + C::EPI);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmY);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs (the leader's copy is used)
+      mbar_init(&rbar[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pt = cid; pt < p.pair_tiles; pt += ncl) {
+        TileCoord tc;
+        decode2(p, pt, (int)rank, BN, tc);
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          const int tap = kb / p.cblocks, cb = kb % p.cblocks;
+          const int dx = tap % p.kw, dy = (tap / p.kw) % p.kh, dt = tap / (p.kw * p.kh);
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (p.a_bytes + C::B_BYTES));
+          const uint32_t bar0 = cluster_addr(&full[stage], 0);
+          tma_load_5d_cg2(sA + stage * C::A_BYTES, &tmX, bar0, cb * BK, tc.x0 + dx - p.pw,
+                          tc.y0 + dy - p.ph, tc.t + dt - p.pt, tc.b);
+          tma_load_2d_cg2_nohint(sB + stage * C::B_BYTES, &tmW, bar0, kb * BK, tc.n0 + (int)rank * (BN / 2));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA (leader CTA)
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int pt = cid; pt < p.pair_tiles; pt += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * ACC_STRIDE;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a = smem_u32(sA + stage * C::A_BYTES), b = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_ss_cg2(d, make_sdesc_sw128(a + 32 * k), make_sdesc_sw128(b + 32 * k), idesc,
+                               (kb | k) != 0);
+            umma_commit_cg2_mc(&empty[stage]);
+            if (kb == p.k_blocks - 1) umma_commit_cg2_mc(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {  // ------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - 4;
+    const int rit = ew * 32 + lane;
+    const bool elected = ew == 0 && lane == 0;
+    constexpr int NS = BN / 64;
+    int acc = 0, cnt = 0;
+    uint32_t acc_phase = 0;
+    if (RES && elected && cid < p.pair_tiles) {
+      TileCoord c0;
+      decode2(p, cid, (int)rank, BN, c0);
+      mbar_arrive_expect_tx(&rbar[0], p.a_bytes);
+      tma_load_5d(sE, &tmR, &rbar[0], c0.n0, c0.x0, c0.y0, c0.t, c0.b);
+    }
+    for (int pt = cid; pt < p.pair_tiles; pt += ncl) {
+      TileCoord tc;
+      const bool real = decode2(p, pt, (int)rank, BN, tc);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * ACC_STRIDE;
+      const uint32_t tcl = cluster_addr(&tempty[acc], 0);
+#pragma unroll 1
+      for (int sub = 0; sub < NS; ++sub) {
+        const int buf = cnt & 1;
+        uint8_t* sb = sE + buf * 16384;
+        const uint32_t sbase = smem_u32(sb);
+        if (elected) {
+          if (RES) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            const int npt = sub + 1 < NS ? pt : pt + ncl;
+            if (npt < p.pair_tiles) {
+              TileCoord c1 = tc;
+              if (sub + 1 >= NS) decode2(p, npt, (int)rank, BN, c1);
+              const int nsub = sub + 1 < NS ? sub + 1 : 0;
+              mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
+              tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
+                          c1.y0, c1.t, c1.b);
+            }
+          } else {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (RES) mbar_wait(&rbar[buf], (cnt >> 1) & 1);
+        uint32_t r[64];
+        ld32(taddr + sub * 64, r);
+        ld32(taddr + sub * 64 + 32, r + 32);
+        tmem_ld_wait();
+        if (sub == NS - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 31) mbar_arrive_cl_relaxed(tcl);
+        }
+        const int col0 = tc.n0 + sub * 64;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[8 * j + e]);
+          if (p.bias) {
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + 8 * j) + 1);
+            v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+            v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+          }
+          const uint32_t a = sbase + sw128(rit, j);
+          if (RES) {
+            const uint4 q = lds4(a);
+            const float2 f0 = unpack_bf16(q.x), f1 = unpack_bf16(q.y), f2 = unpack_bf16(q.z),
+                         f3 = unpack_bf16(q.w);
+            v[0] += f0.x; v[1] += f0.y; v[2] += f1.x; v[3] += f1.y;
+            v[4] += f2.x; v[5] += f2.y; v[6] += f3.x; v[7] += f3.y;
+          }
+          sts4(a, pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+               pack_bf16(v[6], v[7]));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (elected && real) {
+          tma_store_5d(&tmY, sb, col0, tc.x0, tc.y0, tc.t, tc.b);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++cnt;
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
 }
 
 template <int BN, bool RES>
@@ -327,7 +573,14 @@ static bool map_act(CUtensorMap* m, const void* base, int B, int T, int H, int W
 
 template <int BN, bool RES>
 static int launch(const CUtensorMap& x, const CUtensorMap& w, const CUtensorMap& y,
-                  const CUtensorMap& r, const Params& p, int grid, cudaStream_t s) {
+                  const CUtensorMap& r, const Params& p, int grid, bool pair, cudaStream_t s) {
+  if (pair) {
+    using C = Cfg2<BN, RES>;
+    static size_t attr2[64] = {};
+    ensure_smem((const void*)conv2_kernel<BN, RES>, C::SMEM, attr2);
+    conv2_kernel<BN, RES><<<grid, THREADS, C::SMEM, s>>>(x, w, y, r, p);
+    return check_cuda("conv2_kernel");
+  }
   using C = Cfg<BN, RES>;
   static size_t attr[64] = {};
   ensure_smem((const void*)conv_kernel<BN, RES>, C::SMEM, attr);
@@ -335,10 +588,24 @@ static int launch(const CUtensorMap& x, const CUtensorMap& w, const CUtensorMap&
   return check_cuda("conv_kernel");
 }
 
+static int g_conv_pair = -1;  // DDIT_CONV_2CTA=0: 1-CTA tiles only
+static bool conv_pair_enabled() {
+  if (g_conv_pair < 0) {
+    const char* e = getenv("DDIT_CONV_2CTA");
+    g_conv_pair = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_conv_pair != 0;
+}
+
 }  // namespace conv
 }  // namespace ddit
 
 using namespace ddit;
+
+extern "C" DDIT_API int ddit_set_conv_2cta(int on) {
+  conv::g_conv_pair = on ? 1 : 0;
+  return DDIT_OK;
+}
 
 extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
   using namespace conv;
@@ -369,6 +636,8 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
   p.cblocks = a->Cin / 64;
   p.k_blocks = a->kt * a->kh * a->kw * p.cblocks;
   p.a_bytes = p.Wt * p.R * 128;
+  p.pix_tiles = a->B * a->T * p.y_tiles * p.x_tiles;
+  p.pair_tiles = ((p.pix_tiles + 1) / 2) * p.n_tiles;
   p.bias = a->bias;
   CUtensorMap tx, tw, ty, tr;
   memset(&tr, 0, sizeof tr);
@@ -379,7 +648,9 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
     const int K = p.k_blocks * 64;
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)a->Cout};
     cuuint64_t st[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)bn};
+    // CTA pairs load half the weight rows each
+    const bool pair = conv_pair_enabled() && p.pair_tiles >= num_sms() / 2;
+    cuuint32_t box[2] = {64, (cuuint32_t)(pair ? bn / 2 : bn)};
     cuuint32_t es[2] = {1, 1};
     ok = ok && encoder()(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->w), dims, st,
                          box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -391,12 +662,14 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
     return DDIT_E_TMA;
   }
   if (!a->residual) tr = ty;
-  const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+  const bool pair = conv_pair_enabled() && p.pair_tiles >= num_sms() / 2;
+  const int grid = pair ? 2 * (p.pair_tiles < num_sms() / 2 ? p.pair_tiles : num_sms() / 2)
+                        : (p.num_tiles < num_sms() ? p.num_tiles : num_sms());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool res = a->residual != nullptr;
   switch (bn) {
-    case 256: return res ? launch<256, true>(tx, tw, ty, tr, p, grid, s) : launch<256, false>(tx, tw, ty, tr, p, grid, s);
-    case 128: return res ? launch<128, true>(tx, tw, ty, tr, p, grid, s) : launch<128, false>(tx, tw, ty, tr, p, grid, s);
-    default: return res ? launch<64, true>(tx, tw, ty, tr, p, grid, s) : launch<64, false>(tx, tw, ty, tr, p, grid, s);
+    case 256: return res ? launch<256, true>(tx, tw, ty, tr, p, grid, pair, s) : launch<256, false>(tx, tw, ty, tr, p, grid, pair, s);
+    case 128: return res ? launch<128, true>(tx, tw, ty, tr, p, grid, pair, s) : launch<128, false>(tx, tw, ty, tr, p, grid, pair, s);
+    default: return res ? launch<64, true>(tx, tw, ty, tr, p, grid, pair, s) : launch<64, false>(tx, tw, ty, tr, p, grid, pair, s);
   }
 }

@@ -14,6 +14,7 @@
 // M and K tails on load and clips on store), K in {288, 1152, 4096, 4608}, N % BN == 0.
 #include "common.cuh"
 #include "gemm_sm100.cuh"
+#include "cta_pair.cuh"
 
 #include <cstdio>
 #include <cstring>
@@ -247,31 +248,6 @@ DDIT_DEV void resid_issue(const ResidStream& rs, int ns, int j, int row_off, con
     mbar_arrive_expect_tx(&wbar[slot], 4096);
     tma_load_2d(wbase + slot * 4096, tmR, &wbar[slot], c0, m0 + row_off);
   }
-}
-
-DDIT_DEV void mbar_arrive_cl(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
-               : "memory");
-}
-// accumulator hand-back (TMEM empty): no memory to publish -- the tcgen05.wait::ld before and
-// tcgen05.fence::before_thread_sync order the TMEM reads -- so a relaxed arrive; a release arrive
-// would wait for the thread's (and, through the fence, the warp's) outstanding bulk stores
-DDIT_DEV void mbar_arrive_cl_relaxed(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
-               : "memory");
-}
-DDIT_DEV uint32_t cluster_addr(const void* p, uint32_t rank) {
-  uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
-  return a;
-}
-DDIT_DEV uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-DDIT_DEV void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ epilogue: bf16 / gelu / f32
@@ -877,30 +853,6 @@ struct GemmCfg2 {
   static_assert(BN % 16 == 0 && (BN / 2) % 8 == 0 && BN <= 256, "invalid UMMA N for cta_group::2");
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
-
-DDIT_DEV void tma_load_2d_cg2(void* smem_dst, const void* tmap, uint32_t bar_leader, int c0, int c1,
-                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
-}
-DDIT_DEV void umma_bf16_ss_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-DDIT_DEV void umma_commit_cg2_mc(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
 
 // WIDE = 2: each tile is 256 x 2BN, computed as two N = BN MMAs per k-step into the two TMEM
 // accumulator halves [0, BN) and [BN, 2BN) (one tile in flight, no double buffer): per k-block the

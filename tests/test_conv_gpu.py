@@ -45,3 +45,31 @@ def test_conv_matches_torch(cuda, B, T, H, W, Cin, Cout, k, with_res):
     ref = ref_conv(x, w, bias, res, True)
     torch.cuda.synchronize()
     assert rel_l2(y, ref) < 1e-2
+
+
+@pytest.mark.parametrize("B,T,H,W,Cin,Cout,k", [
+    (1, 3, 61, 107, 128, 256, (1, 3, 3)),    # 183 pixel tiles: the last pair has a lone tile
+    (1, 4, 30, 54, 256, 128, (3, 3, 3)),     # causal 3-D, 2 rows per tile
+    (2, 2, 45, 80, 64, 64, (1, 3, 3)),       # BN 64: 32 weight rows per CTA
+])
+@pytest.mark.parametrize("with_res", [False, True])
+def test_conv_cta_pairs_bit_identical(cuda, B, T, H, W, Cin, Cout, k, with_res):
+    """cta_group::2 conv tiles (pairs of 128-pixel tiles, half the weight rows per CTA) against
+    the 1-CTA kernel, bit for bit, and against torch fp32."""
+    from paper_2506_13497_b200 import _lib, kernels
+
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(B, T, H, W, Cin, generator=g).to(cuda, torch.bfloat16)
+    w = (torch.randn(Cout, *k, Cin, generator=g) / (Cin * k[0] * k[1] * k[2]) ** 0.5).to(cuda, torch.bfloat16)
+    bias = (0.1 * torch.randn(Cout, generator=g)).to(cuda)
+    res = torch.randn(B, T, H, W, Cout, generator=g).to(cuda, torch.bfloat16) if with_res else None
+    ys = []
+    for pair in (1, 0):
+        _lib.lib().ddit_set_conv_2cta(pair)
+        try:
+            ys.append(kernels.conv(x, w, bias=bias, residual=res, causal_time=True))
+        finally:
+            _lib.lib().ddit_set_conv_2cta(1)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], ys[1])
+    assert rel_l2(ys[0], ref_conv(x, w, bias, res, True)) < 1e-2
