@@ -138,6 +138,18 @@ def test_gemm_qkv_epilogue(cuda, rope):
         q, k = rot(q), rot(k)
     ref = torch.stack([q, k, v], 1).view(M, 3 * C)
     assert rel_l2(out, ref) < 5e-3
+    # per-head padded weights (80-row slots, 256 x 240 / 128 x 240 tiles of three whole heads):
+    # the same output bit for bit
+    wp = torch.zeros(3 * H * 80, C, device=cuda, dtype=torch.bfloat16)
+    bp = torch.zeros(3 * H * 80, device=cuda)
+    for h in range(3 * H):
+        wp[h * 80:h * 80 + 72] = w[h * 72:(h + 1) * 72]
+        bp[h * 80:h * 80 + 72] = bias[h * 72:(h + 1) * 72]
+    out_p = torch.empty_like(out)
+    kernels.gemm(a, wp, epi=_lib.EPI_QKV, bias=bp, out=out_p, qnorm_w=qw, knorm_w=kw, hidden=C,
+                 rope_tab=tab if rope else None, rope_T=T, rope_S=S, bn=240)
+    torch.cuda.synchronize()
+    assert torch.equal(out_p, out)
 
 
 @pytest.mark.parametrize("nb,N", [(4, 576), (4, 1152), (3, 1152)])
