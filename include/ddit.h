@@ -119,8 +119,8 @@ typedef struct ddit_attn {
 } ddit_attn;
 
 DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
-/* Short-sequence (T <= 32) temporal attention: q/k/v must be the three sections of one
- * row-major QKV matrix and share one index map; one CTA per (batch, token position). */
+/* Temporal attention (T <= 64 frames; tcgen05): q/k/v must be the three sections of one
+ * row-major QKV matrix and share one index map (heads of one position stacked into 128-row tiles). */
 DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
 /* LayerNorm (no affine, eps) + t2i modulate of the fp32 residual rows:
  * out_bf16[r, :] = LN(x[r, :]) * (1 + scale[b]) + shift[b], b = r / rows_per_b, shift / scale

@@ -1,10 +1,10 @@
-// Temporal self-attention for short sequences (T <= 32 frames) on tcgen05 /
+// Temporal self-attention (T <= 64 frames) on tcgen05 /
 // TMEM, fed by cp.async.
 //
 // The temporal sequences of the DDiT step are the T frames of one token position: rows
 // base + t*tok of the token-major QKV matrix, i.e. one (batch, position, head) is a tiny T x T
 // problem. A work unit packs HG heads of ONE position into a 128-row MMA tile, rows
-// r = i * R + t for head hg * HG + i (R = 16 for T <= 16, 32 for T <= 32; HG = 128 / R).
+// r = i * R + t for head hg * HG + i (R = 16 for T <= 16, 32 for T <= 32, 64 for T <= 64; HG = 128 / R).
 //
 //   loads     : four loader warps copy the unit's q / k / v slices with 16 B cp.async straight
 //               into the 128B-swizzled (columns 0..63) and 32B-swizzled (64..79) K-major operand
@@ -344,8 +344,14 @@ __global__ void __launch_bounds__(ta::THREADS, 1)
       const int b = n & 1;
       mbar_wait(&s_full[b], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t s[32];
-      tmem_ld_32x32b_x32(lane_base + TM_S + 128 * b + 32 * q, s);
+      // the row's R keys: S columns [R (row / R), + R) -- inside the warp's 32 columns for R <= 32,
+      // the 64 columns of its head block for R = 64
+      constexpr int NL = R == 64 ? 64 : 32;
+      uint32_t s[NL];
+      const uint32_t scol = R == 64 ? 64u * (q >> 1) : 32u * q;
+      tmem_ld_32x32b_x32(lane_base + TM_S + 128 * b + scol, *reinterpret_cast<uint32_t(*)[32]>(s));
+      if constexpr (R == 64)
+        tmem_ld_32x32b_x32(lane_base + TM_S + 128 * b + scol + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(ta::THREADS, 1)
         for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(hi ? s[16 + j] : s[j]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(s[j]);
+        for (int j = 0; j < R; ++j) v[j] = __uint_as_float(s[j]);
       }
       float mx = -INFINITY;
 #pragma unroll
@@ -374,7 +380,8 @@ __global__ void __launch_bounds__(ta::THREADS, 1)
         l += e0 + e1;
         pk[j / 2] = pack_bf16(e0, e1);
       }
-      uint32_t w[16];
+      constexpr int NW = R == 64 ? 32 : 16;  // packed P columns this warp writes
+      uint32_t w[NW];
       if constexpr (R == 16) {
         const bool hi = lane >= 16;
 #pragma unroll
@@ -384,12 +391,17 @@ __global__ void __launch_bounds__(ta::THREADS, 1)
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) w[i] = pk[i];
+        for (int i = 0; i < NW; ++i) w[i] = pk[i];
       }
       // the previous unit's PV has read P (and produced its O)
       if (n >= 1) mbar_wait(&pv_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
       tc_fence_after();
-      ta::tmem_st16(lane_base + TM_P + 16 * q, w);
+      if constexpr (R == 64) {
+        ta::tmem_st16(lane_base + TM_P + 32 * (q >> 1), w);
+        ta::tmem_st16(lane_base + TM_P + 32 * (q >> 1) + 16, w + 16);
+      } else {
+        ta::tmem_st16(lane_base + TM_P + 16 * q, w);
+      }
       ta::tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -431,19 +443,19 @@ int temporal_plan_init(TemporalPlan* tp, const ddit_attn* a) {
   const int C = a->heads * a->head_dim;
   const auto* q = static_cast<const __nv_bfloat16*>(a->q);
   const int inner = a->q_inner > 1 ? a->q_inner : 1;
-  if (a->head_dim != 72 || a->Lq != a->Lk || a->Lq < 1 || a->Lq > 32 || a->ldq != 3 * C ||
+  if (a->head_dim != 72 || a->Lq != a->Lk || a->Lq < 1 || a->Lq > 64 || a->ldq != 3 * C ||
       static_cast<const __nv_bfloat16*>(a->k) != q + C ||
       static_cast<const __nv_bfloat16*>(a->v) != q + 2 * C || a->ldk != a->ldq ||
       a->ldv != a->ldq || (a->q_inner > 1 && a->q_inner_stride != 1) || a->kv_tok != a->q_tok ||
       a->kv_outer != a->q_outer || a->kv_inner != a->q_inner || a->num_seqs % inner ||
       a->ldo % 8 || (reinterpret_cast<uintptr_t>(a->q) & 15) ||
       (reinterpret_cast<uintptr_t>(a->o) & 15)) {
-    set_error("temporal attention: needs one QKV matrix, T <= 32, shared q/kv index map");
+    set_error("temporal attention: needs one QKV matrix, T <= 64, shared q/kv index map");
     return DDIT_E_INVALID;
   }
   memset(tp, 0, sizeof *tp);
   const int T = a->Lq;
-  const int R = T <= 16 ? 16 : 32, HG = 128 / R;
+  const int R = T <= 16 ? 16 : T <= 32 ? 32 : 64, HG = 128 / R;
   const int batches = a->num_seqs / inner;
   {
     static PFN_encode_ta enc = ta_encoder();
@@ -479,9 +491,9 @@ int temporal_plan_init(TemporalPlan* tp, const ddit_attn* a) {
 }
 
 int temporal_plan_launch(const TemporalPlan* tp, cudaStream_t s) {
-  static size_t attr[2][64] = {};
-  auto kern = tp->R == 16 ? temporal_tc_kernel<16> : temporal_tc_kernel<32>;
-  ensure_smem((const void*)kern, ta::SMEM, attr[tp->R == 32]);
+  static size_t attr[3][64] = {};
+  auto kern = tp->R == 16 ? temporal_tc_kernel<16> : tp->R == 32 ? temporal_tc_kernel<32> : temporal_tc_kernel<64>;
+  ensure_smem((const void*)kern, ta::SMEM, attr[tp->R == 16 ? 0 : tp->R == 32 ? 1 : 2]);
   launch_pdl(kern, tp->grid, dim3(ta::THREADS), ta::SMEM, s, tp->p);
   return check_cuda("temporal_tc_kernel");
 }

@@ -397,7 +397,7 @@ int attn(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
   return timed(r, K_ATTN, s, 1, [&] { return attention_launch(a, s); });
 }
 int attn_temporal(ddit_req* r, int k, const ddit_attn* a, cudaStream_t s) {
-  if (a->Lq > 32) return attn(r, a, s);
+  if (a->Lq > 64) return attn(r, a, s);
   if (!r->tm_self_ok[k]) {
     set_error("block %d: temporal attention plan missing", k);
     return DDIT_E_CONFIG;
@@ -487,7 +487,7 @@ int build_attn_plans(ddit_req* r) {
       if (rc) return rc;
       r->fm_self_ok[k] = 1;
     }
-    if ((k & 1) && a.Lq <= 32) {
+    if ((k & 1) && a.Lq <= 64) {
       int rc = temporal_plan_init(&r->tm_self[k], &a);
       if (rc) return rc;
       r->tm_self_ok[k] = 1;

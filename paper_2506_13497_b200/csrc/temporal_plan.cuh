@@ -13,7 +13,7 @@ struct alignas(64) TemporalParams {
   int ld;                    // QKV row stride (elements)
   long long tok_ld;          // frame stride (elements): tok rows
   int outer;                 // batch stride (rows); positions are consecutive rows
-  int T;              // frames per sequence (<= 32)
+  int T;              // frames per sequence (<= 64)
   int heads;
   int groups;         // head groups of 128 / R heads
   int inner;          // positions per batch
@@ -23,7 +23,7 @@ struct alignas(64) TemporalParams {
 
 struct TemporalPlan {
   TemporalParams p;
-  int R;                      // rows per head in a tile: 16 (T <= 16) or 32
+  int R;                      // rows per head in a tile: 16 (T <= 16), 32 (T <= 32) or 64
   dim3 grid;
 };
 
