@@ -27,9 +27,6 @@
 
 #include "fmha_plan.cuh"
 #include "temporal_plan.cuh"
-namespace ddit {
-int attention_launch(const ddit_attn* a, cudaStream_t s);
-}
 
 using namespace ddit;
 typedef __nv_bfloat16 bf16;
@@ -393,13 +390,12 @@ int ln_mod(ddit_req* r, float* x, int M, const float* shift, const float* scale,
     return (int)DDIT_OK;
   });
 }
-int attn(ddit_req* r, const ddit_attn* a, cudaStream_t s) {
-  return timed(r, K_ATTN, s, 1, [&] { return attention_launch(a, s); });
-}
+// Temporal self-attention runs the tcgen05 plan built at request open (T <= 64 latent frames,
+// i.e. every OpenSora clip length); there is no other kernel for it on the step path.
 int attn_temporal(ddit_req* r, int k, const ddit_attn* a, cudaStream_t s) {
-  if (a->Lq > 64) return attn(r, a, s);
+  (void)a;
   if (!r->tm_self_ok[k]) {
-    set_error("block %d: temporal attention plan missing", k);
+    set_error("block %d: temporal attention plan missing (T <= 64 latent frames supported)", k);
     return DDIT_E_CONFIG;
   }
   const TemporalPlan& tp = r->tm_self[k];
@@ -487,7 +483,7 @@ int build_attn_plans(ddit_req* r) {
       if (rc) return rc;
       r->fm_self_ok[k] = 1;
     }
-    if ((k & 1) && a.Lq <= 64) {
+    if (k & 1) {  // T > 64 latent frames: the request cannot open (no other temporal kernel)
       int rc = temporal_plan_init(&r->tm_self[k], &a);
       if (rc) return rc;
       r->tm_self_ok[k] = 1;
