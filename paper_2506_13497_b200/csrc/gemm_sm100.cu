@@ -1265,8 +1265,19 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
   p->ep = ep;
   // 256 x 384 tiles only where the long K loop hides the un-overlapped epilogue (fc2, K = 4608:
   // 94.0 -> 91.3 us; at K = 1152 they lose 13-16 %, scripts/wide_probe.py); bit-identical results
+  gemm_plan_refresh(p);
+  return 0;
+}
+
+// Tile shape and launch grid from the plan's current epilogue parameters (an exchange attached
+// after the plan was built turns the reduce-add into load / update / store, which has no wide
+// tile): called at plan build and by the runtime after it edits a plan's EpiParams.
+void gemm_plan_refresh(GemmPlan* p) {
+  if (p->bn <= 0 || p->M <= 0) return;  // never built (a rank without rows in this layout)
+  const int M = p->M, N = p->N, K = p->K, bn = p->bn, epi = p->epi;
+  const bool red = epi == EPI_RESID_RED && !p->ep.xch && !p->ep.out2;
   p->wide = p->two_cta && bn == 192 && N % (2 * bn) == 0 && K >= 4096 && gemm_wide_enabled() &&
-            (epi == EPI_RESID_RED || epi == EPI_BF16) && !ep.xch;
+            (red || epi == EPI_BF16) && !p->ep.xch;
   if (p->two_cta) {
     const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / (bn * (p->wide ? 2 : 1)));
     const int clusters = num_sms() / 2;
@@ -1275,7 +1286,6 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
     const int tiles = ((M + BM - 1) / BM) * (N / bn);
     p->grid = tiles < num_sms() ? tiles : num_sms();
   }
-  return 0;
 }
 
 static int g_resid_red = -1;

@@ -76,6 +76,8 @@ int gemm_plan_init_cta(GemmPlan* p, const void* A, int lda, const void* B, int l
 // BN and 1-/2-CTA tiles for an M x N output (fills the GPU at small M; bit-identical results)
 void gemm_pick_tile(int M, int N, int epi, int* bn, int* two_cta);
 int gemm_plan_launch(const GemmPlan* p, cudaStream_t stream);
+// recompute the tile shape / grid after editing p->ep (e.g. attaching the DSP exchange)
+void gemm_plan_refresh(GemmPlan* p);
 int num_sms();
 bool two_cta_enabled();
 bool gemm_wide_enabled();

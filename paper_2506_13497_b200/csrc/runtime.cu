@@ -944,9 +944,13 @@ DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const*
   const Geometry& g = r->g;
   r->fused_xch = g.P > 1 && fused_exchange_enabled();
   for (int k = 0; k < 2 * r->m->cfg.depth && !r->plans.empty(); ++k) {
-    EpiParams& e = r->plans[(size_t)k * G_N + G_FC2].ep;
+    GemmPlan& fc2 = r->plans[(size_t)k * G_N + G_FC2];
+    EpiParams& e = fc2.ep;
     e.xch = 0;
-    if (!r->fused_xch) continue;
+    if (!r->fused_xch) {
+      gemm_plan_refresh(&fc2);
+      continue;
+    }
     const bool temporal = k & 1;
     e.xch = temporal ? 2 : 1;
     for (int q = 0; q < kMaxDop; ++q) {
@@ -963,6 +967,7 @@ DDIT_API int ddit_request_set_peers(ddit_req* r, void* const* x_sp, void* const*
     e.xcounter = r->counter;
     e.xepoch = r->counter + 1;
     e.xrank = g.rank;
+    gemm_plan_refresh(&fc2);  // the exchange epilogue has no wide tile
   }
   return DDIT_OK;
 }
