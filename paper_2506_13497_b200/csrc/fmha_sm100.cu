@@ -646,7 +646,9 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
         // MUFU turn: the two groups' exps phases alternate (g0 tile j, g1 tile j, g0 tile j+1, ...)
         // so each runs at the full SFU rate while the other does its max / P stores / waits,
         // instead of both contending in phase
-        if (has1) mbar_wait(&exp_tok[g], (tk & 1) ^ (g == 0 ? 1 : 0));
+        // (the ragged last tile of a unit -- a few keys -- runs outside the turn order: both groups
+        // skip it, so the alternation stays in step; cross attention 34.6 -> 34.1 us)
+        if (has1 && full) mbar_wait(&exp_tok[g], (tk & 1) ^ (g == 0 ? 1 : 0));
         if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 1);
         // exps first (packed bf16 P kept in the consumed s[] registers: chunk c -> s[4c..4c+3]),
         // so the MUFU work overlaps the tensor core finishing PV_{j-1}
@@ -697,7 +699,7 @@ __global__ void __launch_bounds__(fm::THREADS, 1)
           }
         }
         if (trc) FM_TRACE(g * 512 + (n & 63) * 8 + 2);
-        if (has1) {  // hand the MUFU turn to the other group
+        if (has1 && full) {  // hand the MUFU turn to the other group
           __syncwarp();
           if (lane == 31) mbar_arrive_relaxed(&exp_tok[g ^ 1]);
           ++tk;
