@@ -59,6 +59,9 @@ DDIT_API int ddit_set_qkv_pad(int on);
 /* VAE convolutions as cta_group::2 pairs of 128-pixel tiles (half the weight rows per CTA) when
  * there are enough tiles (default 1; env DDIT_CONV_2CTA=0); bit-identical results. */
 DDIT_API int ddit_set_conv_2cta(int on);
+/* VAE convolution pixel tiles: R rows x Wt columns chosen per layer for the fewest tiles (1,
+ * default; env DDIT_CONV_TILES=0: 128-pixel rows); bit-identical results. */
+DDIT_API int ddit_set_conv_tile_search(int on);
 /* Programmatic dependent launch of the step kernels (default 1; env DDIT_PDL=0). */
 DDIT_API int ddit_set_pdl(int on);
 /* One process driving several GPUs: let `device` access `peer`'s memory (idempotent). */

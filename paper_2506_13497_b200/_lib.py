@@ -129,6 +129,7 @@ _SIGNATURES = {
     "ddit_set_gemm_wide": [ci],
     "ddit_set_qkv_pad": [ci],
     "ddit_set_conv_2cta": [ci],
+    "ddit_set_conv_tile_search": [ci],
     "ddit_set_pdl": [ci],
     "ddit_set_fused_exchange": [ci],
     "ddit_set_resid_reduce": [ci],

@@ -21,6 +21,7 @@
 #include "ddit.h"
 #include "capi_internal.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -588,6 +589,15 @@ static int launch(const CUtensorMap& x, const CUtensorMap& w, const CUtensorMap&
   return check_cuda("conv_kernel");
 }
 
+static int g_conv_tiles = -1;  // DDIT_CONV_TILES=0: 128-pixel rows (W >= 128) / whole rows
+static bool conv_tile_search_enabled() {
+  if (g_conv_tiles < 0) {
+    const char* e = getenv("DDIT_CONV_TILES");
+    g_conv_tiles = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_conv_tiles != 0;
+}
+
 static int g_conv_pair = -1;  // DDIT_CONV_2CTA=0: 1-CTA tiles only
 static bool conv_pair_enabled() {
   if (g_conv_pair < 0) {
@@ -601,6 +611,11 @@ static bool conv_pair_enabled() {
 }  // namespace ddit
 
 using namespace ddit;
+
+extern "C" DDIT_API int ddit_set_conv_tile_search(int on) {
+  conv::g_conv_tiles = on ? 1 : 0;
+  return DDIT_OK;
+}
 
 extern "C" DDIT_API int ddit_set_conv_2cta(int on) {
   conv::g_conv_pair = on ? 1 : 0;
@@ -625,10 +640,29 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
   p.pt = a->causal_time ? a->kt - 1 : a->kt / 2;
   p.ph = a->kh / 2;
   p.pw = a->kw / 2;
-  p.Wt = a->W < 128 ? a->W : 128;
-  p.R = p.Wt == a->W ? 128 / a->W : 1;
-  if (p.R > a->H) p.R = a->H;
-  if (p.R < 1) p.R = 1;
+  // pixel tile = R rows x Wt columns (Wt * R <= 128, the MMA's M): the shape with the fewest
+  // tiles per frame, i.e. the least MMA work on pixels past the frame edge (e.g. W = 432:
+  // 16 x 8 tiles, 810 per 240-row frame, instead of 128 x 1, 960); ties keep the wider rows.
+  // Results do not depend on the tiling (same K order per pixel).
+  {
+    auto tiles_of = [&](int wt, int r) {
+      return (long)((a->W + wt - 1) / wt) * ((a->H + r - 1) / r);
+    };
+    int bw = a->W < 128 ? a->W : 128;
+    int br = std::max(1, std::min(a->H, 128 / bw));
+    if (conv_tile_search_enabled()) {
+      for (int wt : {128, 64, 32, 16}) {
+        if (wt > a->W) continue;
+        const int r = std::max(1, std::min(a->H, 128 / wt));
+        if (tiles_of(wt, r) < tiles_of(bw, br)) {
+          bw = wt;
+          br = r;
+        }
+      }
+    }
+    p.Wt = bw;
+    p.R = br;
+  }
   p.x_tiles = (a->W + p.Wt - 1) / p.Wt;
   p.y_tiles = (a->H + p.R - 1) / p.R;
   p.n_tiles = a->Cout / bn;

@@ -73,3 +73,25 @@ def test_conv_cta_pairs_bit_identical(cuda, B, T, H, W, Cin, Cout, k, with_res):
     torch.cuda.synchronize()
     assert torch.equal(ys[0], ys[1])
     assert rel_l2(ys[0], ref_conv(x, w, bias, res, True)) < 1e-2
+
+
+@pytest.mark.parametrize("H,W,Cin,Cout", [(24, 432, 128, 128), (30, 216, 64, 256), (12, 108, 256, 64)])
+def test_conv_tile_shapes_bit_identical(cuda, H, W, Cin, Cout):
+    """Per-layer pixel-tile shapes (16 x 8, 32 x 4, ... chosen for the fewest tiles) against the
+    128-pixel-row tiles, bit for bit."""
+    from paper_2506_13497_b200 import _lib, kernels
+
+    g = torch.Generator().manual_seed(2)
+    x = torch.randn(2, 1, H, W, Cin, generator=g).to(cuda, torch.bfloat16)
+    w = (torch.randn(Cout, 1, 3, 3, Cin, generator=g) / (Cin * 9) ** 0.5).to(cuda, torch.bfloat16)
+    bias = (0.1 * torch.randn(Cout, generator=g)).to(cuda)
+    ys = []
+    for search in (1, 0):
+        _lib.lib().ddit_set_conv_tile_search(search)
+        try:
+            ys.append(kernels.conv(x, w, bias=bias, causal_time=False))
+        finally:
+            _lib.lib().ddit_set_conv_tile_search(1)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], ys[1])
+    assert rel_l2(ys[0], ref_conv(x, w, bias, None, False)) < 1e-2
