@@ -314,8 +314,18 @@ typedef struct ddit_conv_args {
   int B, T, H, W, Cin, Cout;
   int kt, kh, kw;
   int causal_time;
+  /* optional (NULL = off): GroupNorm statistics of y for gn_groups groups, written by the
+   * epilogue as fp32 (sum, sum of squares) pairs over the in-frame pixels of each pixel tile:
+   * per frame [B*T][gn_groups][nblk], nblk = ddit_conv_frame_tiles(H, W), or with gn_per_sample
+   * per sample [B][gn_groups][T*nblk]; the input of ddit_groupnorm_partials. Needs
+   * Cout / gn_groups in {2, 4, 8, 16, 32, 64}. */
+  float* gn_part;
+  int gn_groups;
+  int gn_per_sample;
 } ddit_conv_args;
 DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream);
+/* pixel tiles per H x W frame of ddit_conv (the nblk of its GroupNorm partials) */
+DDIT_API int ddit_conv_frame_tiles(int H, int W);
 
 /* GroupNorm over channels-last x [N][P][C] bf16 (per sample n, group of C/G channels, all P
  * pixels), affine, optional SiLU -> y bf16. Deterministic (fixed reduction order).
@@ -324,6 +334,12 @@ DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream);
 DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* gamma,
                             const float* beta, int N, int P, int C, int G, float eps, int silu_act,
                             void* stream);
+/* The same GroupNorm from statistics partials [N][G][nblk] (sum, sum of squares) that the
+ * producing ddit_conv wrote (gn_part): no statistics pass over x. coef: device scratch of N*C
+ * float2. */
+DDIT_API int ddit_groupnorm_partials(const void* x, void* y, const float* partial, int nblk,
+                                     float* coef, const float* gamma, const float* beta, int N,
+                                     int P, int C, int G, float eps, int silu_act, void* stream);
 /* nearest 2x in H and W: [N][H][W][C] -> [N][2H][2W][C] bf16 */
 DDIT_API int ddit_upsample2x(const void* x, void* y, int N, int H, int W, int C, void* stream);
 /* OpenSora temporal upsampling: [B][T][HW][2C] (channel 2c+ts) -> [B][2T][HW][C] bf16 */

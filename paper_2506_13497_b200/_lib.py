@@ -105,6 +105,7 @@ class ConvArgs(ctypes.Structure):
         ("x", vp), ("y", vp), ("w", vp), ("bias", vp), ("residual", vp),
         ("B", ci), ("T", ci), ("H", ci), ("W", ci), ("Cin", ci), ("Cout", ci),
         ("kt", ci), ("kh", ci), ("kw", ci), ("causal_time", ci),
+        ("gn_part", vp), ("gn_groups", ci), ("gn_per_sample", ci),
     ]
 
 
@@ -168,6 +169,8 @@ _SIGNATURES = {
     "ddit_request_profile_read": [vp, ctypes.POINTER(cf), ctypes.POINTER(ci)],
     "ddit_conv": [ctypes.POINTER(ConvArgs), vp],
     "ddit_groupnorm": [vp, vp, vp, vp, vp, ci, ci, ci, ci, cf, ci, vp],
+    "ddit_conv_frame_tiles": [ci, ci],
+    "ddit_groupnorm_partials": [vp, vp, vp, ci, vp, vp, vp, ci, ci, ci, ci, cf, ci, vp],
     "ddit_upsample2x": [vp, vp, ci, ci, ci, ci, vp],
     "ddit_depth_to_time": [vp, vp, ci, ci, ci, ci, vp],
     "ddit_frames_out": [vp, vp, ci, ci, ci, ci, ci, ci, ci, vp],

@@ -38,9 +38,10 @@ struct Cfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EPI = 2 * 16384;  // staging (64 bf16 channels x 128 rows, SW128) x 2
   static constexpr int BAR = 256;
-  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - EPI) / STAGE;
+  static constexpr int GNR = 1024;  // GroupNorm statistics: per-warp channel-pair sums [4][8][4][2] fp32
+  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - GNR - EPI) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR + GNR;
 };
 
 template <int BN, bool RES>
@@ -50,9 +51,10 @@ struct Cfg2 {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EPI = 2 * 16384;
   static constexpr int BAR = 256;
-  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - EPI) / STAGE;
+  static constexpr int GNR = 1024;
+  static constexpr int STAGES_RAW = (232448 - 1024 - BAR - GNR - EPI) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + BAR + GNR;
   static_assert(B_BYTES % 1024 == 0, "B half-tile must keep 1024 B swizzle-atom alignment");
 };
 
@@ -64,6 +66,12 @@ struct Params {
   int a_bytes;
   int pix_tiles, pair_tiles;  // 2-CTA: pixel tiles, and (pixel-tile pair, channel block) tiles
   const float* bias;
+  // optional per-frame GroupNorm statistics of the output: (sum, sum of squares) of group g over
+  // the in-frame pixels of pixel tile `slot` of frame n = b T + t -> gn_part[(n G + g) nblk + slot],
+  // nblk = x_tiles * y_tiles (the partials gn_finalize_kernel reduces)
+  float2* gn_part;
+  int gn_G, gn_cg;
+  int gn_per_sample;  // 1: statistics per sample b over all T frames, slot = (t y_tiles + yt) x_tiles + xt
 };
 
 DDIT_DEV void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
@@ -128,6 +136,92 @@ DDIT_DEV TileCoord decode(const Params& p, int tile, int BN) {
   return c;
 }
 
+// GroupNorm statistics of the staged 128 x 64 bf16 output sub-tiles (channels col0 .. col0 + 63,
+// rows = the tile's pixels, SW128 rows of 128 B). add(): thread t sums 16 B chunk t % 8 of rows
+// 8 (t / 8) .. + 7 (in-frame pixels only, `mask`) per channel pair, a fixed xor tree joins the
+// warp's four row sets and lanes 0-7 leave the warp's sums in `red`; flush() -- after the
+// epilogue's next named barrier, so no barrier of its own -- joins the four warps in warp order
+// and stores one (sum, sum of squares) per group: a deterministic reduction, the same in the
+// 1-CTA and the CTA-pair kernel. One `red` suffices: the epilogue has two barriers per sub-tile,
+// flush() reads before the second, the next add() writes after it.
+DDIT_DEV int gn_nblk(const Params& p) { return p.x_tiles * p.y_tiles * (p.gn_per_sample ? p.T : 1); }
+
+struct GnStats {
+  int mask = 0;        // this thread's 8 rows that are in-frame pixels of the current tile
+  bool pending = false;
+  size_t pidx = 0;     // gn_part index of group col0 / cg of the pending sub-tile
+  bool preal = false;
+
+  DDIT_DEV void tile(const Params& p, const TileCoord& tc, int rit) {
+    mask = 0;
+    const int npix = p.Wt * p.R;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = (rit >> 3) * 8 + i;
+      const int yy = tc.y0 + r / p.Wt, xx = tc.x0 + r % p.Wt;
+      if (r < npix && yy < p.H && xx < p.W) mask |= 1 << i;
+    }
+  }
+  DDIT_DEV void add(const Params& p, uint32_t sbase, float* red, int rit, const TileCoord& tc,
+                    int col0, bool real) {
+    const int j = rit & 7, rs = rit >> 3;
+    float sm[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (mask >> i & 1) {
+        const uint4 q = lds4(sbase + sw128(rs * 8 + i, j));
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 a = unpack_bf16(w4[k]);
+          sm[k] += a.x + a.y;
+          sq[k] = fmaf(a.x, a.x, fmaf(a.y, a.y, sq[k]));
+        }
+      }
+    }
+    // the staging buffer's next writer may be a TMA load (residual of a later sub-tile)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        sm[k] += __shfl_xor_sync(0xffffffffu, sm[k], o);
+        sq[k] += __shfl_xor_sync(0xffffffffu, sq[k], o);
+      }
+    if ((rit & 31) < 8) {
+      float* w = red + ((rit >> 5) * 8 + j) * 8;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w[2 * k] = sm[k];
+        w[2 * k + 1] = sq[k];
+      }
+    }
+    pending = true;
+    preal = real;
+    const int slot = (tc.y0 / p.R) * p.x_tiles + tc.x0 / p.Wt;
+    if (p.gn_per_sample)
+      pidx = ((size_t)tc.b * p.gn_G + col0 / p.gn_cg) * gn_nblk(p) + (size_t)tc.t * p.x_tiles * p.y_tiles + slot;
+    else
+      pidx = ((size_t)(tc.b * p.T + tc.t) * p.gn_G + col0 / p.gn_cg) * gn_nblk(p) + slot;
+  }
+  // call after a barrier of all 128 epilogue threads that follows add()
+  DDIT_DEV void flush(const Params& p, const float* red, int rit) {
+    if (!pending) return;
+    pending = false;
+    const int pairs = p.gn_cg / 2, ngrp = 64 / p.gn_cg;
+    if (rit >= ngrp || !preal) return;
+    const float* rb = red;
+    float s = 0.f, q = 0.f;
+    for (int h = rit * pairs; h < (rit + 1) * pairs; ++h)  // channel pair h = chunk h / 4, k = h % 4
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        s += rb[(w * 8 + (h >> 2)) * 8 + 2 * (h & 3)];
+        q += rb[(w * 8 + (h >> 2)) * 8 + 2 * (h & 3) + 1];
+      }
+    p.gn_part[pidx + (size_t)rit * gn_nblk(p)] = make_float2(s, q);
+  }
+};
+
 // pair tile pt, CTA rank r -> pixel tile 2 (pt / n_tiles) + r, channel block pt % n_tiles. A rank
 // without a pixel tile (odd count) gets the last tile moved past the right edge: its loads are all
 // zero fill and it stores nothing (returns false).
@@ -167,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  float* gnred = reinterpret_cast<float*>(sE + C::EPI + C::BAR);
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_rank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -268,9 +363,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_arrive_expect_tx(&rbar[0], p.a_bytes);
       tma_load_5d(sE, &tmR, &rbar[0], c0.n0, c0.x0, c0.y0, c0.t, c0.b);
     }
+    const bool gn = p.gn_part != nullptr;
+    GnStats gs;
     for (int pt = cid; pt < p.pair_tiles; pt += ncl) {
       TileCoord tc;
       const bool real = decode2(p, pt, (int)rank, BN, tc);
+      if (gn) gs.tile(p, tc, rit);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * ACC_STRIDE;
@@ -280,23 +378,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int buf = cnt & 1;
         uint8_t* sb = sE + buf * 16384;
         const uint32_t sbase = smem_u32(sb);
+        // residual of the next sub-tile into the other buffer; with GroupNorm statistics that
+        // buffer may still be read by add() of the previous sub-tile: issue after the barrier
+        auto next_res = [&]() {
+          const int npt = sub + 1 < NS ? pt : pt + ncl;
+          if (npt < p.pair_tiles) {
+            TileCoord c1 = tc;
+            if (sub + 1 >= NS) decode2(p, npt, (int)rank, BN, c1);
+            const int nsub = sub + 1 < NS ? sub + 1 : 0;
+            mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
+            tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
+                        c1.y0, c1.t, c1.b);
+          }
+        };
         if (elected) {
           if (RES) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            const int npt = sub + 1 < NS ? pt : pt + ncl;
-            if (npt < p.pair_tiles) {
-              TileCoord c1 = tc;
-              if (sub + 1 >= NS) decode2(p, npt, (int)rank, BN, c1);
-              const int nsub = sub + 1 < NS ? sub + 1 : 0;
-              mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
-              tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
-                          c1.y0, c1.t, c1.b);
-            }
+            if (!gn) next_res();
           } else {
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (gn) {
+          if (RES && elected) next_res();
+          gs.flush(p, gnred, rit);
+        }
         if (RES) mbar_wait(&rbar[buf], (cnt >> 1) & 1);
         uint32_t r[64];
         ld32(taddr + sub * 64, r);
@@ -336,10 +443,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tma_store_5d(&tmY, sb, col0, tc.x0, tc.y0, tc.t, tc.b);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        if (gn) gs.add(p, sbase, gnred, rit, tc, col0, real);
         ++cnt;
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+    }
+    if (gn) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      gs.flush(p, gnred, rit);
     }
     if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -372,6 +484,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
+  float* gnred = reinterpret_cast<float*>(sE + C::EPI + C::BAR);
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -459,8 +572,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_arrive_expect_tx(&rbar[0], p.a_bytes);
       tma_load_5d(sE, &tmR, &rbar[0], c0.n0, c0.x0, c0.y0, c0.t, c0.b);
     }
+    const bool gn = p.gn_part != nullptr;
+    GnStats gs;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const TileCoord tc = decode(p, tile, BN);
+      if (gn) gs.tile(p, tc, rit);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * ACC_STRIDE;
@@ -469,22 +585,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int buf = cnt & 1;
         uint8_t* sb = sE + buf * 16384;
         const uint32_t sbase = smem_u32(sb);
+        auto next_res = [&]() {  // see conv2_kernel
+          const int nt = sub + 1 < NS ? tile : tile + (int)gridDim.x;
+          if (nt < p.num_tiles) {
+            const TileCoord c1 = sub + 1 < NS ? tc : decode(p, nt, BN);
+            const int nsub = sub + 1 < NS ? sub + 1 : 0;
+            mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
+            tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
+                        c1.y0, c1.t, c1.b);
+          }
+        };
         if (elected) {
           if (RES) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            const int nt = sub + 1 < NS ? tile : tile + (int)gridDim.x;
-            if (nt < p.num_tiles) {
-              const TileCoord c1 = sub + 1 < NS ? tc : decode(p, nt, BN);
-              const int nsub = sub + 1 < NS ? sub + 1 : 0;
-              mbar_arrive_expect_tx(&rbar[buf ^ 1], p.a_bytes);
-              tma_load_5d(sE + (buf ^ 1) * 16384, &tmR, &rbar[buf ^ 1], c1.n0 + nsub * 64, c1.x0,
-                          c1.y0, c1.t, c1.b);
-            }
+            if (!gn) next_res();
           } else {
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (gn) {
+          if (RES && elected) next_res();
+          gs.flush(p, gnred, rit);
+        }
         if (RES) mbar_wait(&rbar[buf], (cnt >> 1) & 1);
         uint32_t r[64];
         ld32(taddr + sub * 64, r);
@@ -524,10 +647,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_store_5d(&tmY, sb, col0, tc.x0, tc.y0, tc.t, tc.b);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        if (gn) gs.add(p, sbase, gnred, rit, tc, col0, true);
         ++cnt;
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+    }
+    if (gn) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      gs.flush(p, gnred, rit);
     }
     if (elected) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -607,6 +735,28 @@ static bool conv_pair_enabled() {
   return g_conv_pair != 0;
 }
 
+// pixel tile = R rows x Wt columns (Wt * R <= 128, the MMA's M): the shape with the fewest tiles
+// per frame, i.e. the least MMA work on pixels past the frame edge (e.g. W = 432: 16 x 8 tiles,
+// 810 per 240-row frame, instead of 128 x 1, 960); ties keep the wider rows. Results do not
+// depend on the tiling (same K order per pixel).
+static void pixel_tile(int H, int W, int* Wt, int* R) {
+  auto tiles_of = [&](int wt, int r) { return (long)((W + wt - 1) / wt) * ((H + r - 1) / r); };
+  int bw = W < 128 ? W : 128;
+  int br = std::max(1, std::min(H, 128 / bw));
+  if (conv_tile_search_enabled()) {
+    for (int wt : {128, 64, 32, 16}) {
+      if (wt > W) continue;
+      const int r = std::max(1, std::min(H, 128 / wt));
+      if (tiles_of(wt, r) < tiles_of(bw, br)) {
+        bw = wt;
+        br = r;
+      }
+    }
+  }
+  *Wt = bw;
+  *R = br;
+}
+
 }  // namespace conv
 }  // namespace ddit
 
@@ -620,6 +770,13 @@ extern "C" DDIT_API int ddit_set_conv_tile_search(int on) {
 extern "C" DDIT_API int ddit_set_conv_2cta(int on) {
   conv::g_conv_pair = on ? 1 : 0;
   return DDIT_OK;
+}
+
+extern "C" DDIT_API int ddit_conv_frame_tiles(int H, int W) {
+  if (H < 1 || W < 1) return 0;
+  int wt = 0, r = 0;
+  conv::pixel_tile(H, W, &wt, &r);
+  return ((W + wt - 1) / wt) * ((H + r - 1) / r);
 }
 
 extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
@@ -640,29 +797,7 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
   p.pt = a->causal_time ? a->kt - 1 : a->kt / 2;
   p.ph = a->kh / 2;
   p.pw = a->kw / 2;
-  // pixel tile = R rows x Wt columns (Wt * R <= 128, the MMA's M): the shape with the fewest
-  // tiles per frame, i.e. the least MMA work on pixels past the frame edge (e.g. W = 432:
-  // 16 x 8 tiles, 810 per 240-row frame, instead of 128 x 1, 960); ties keep the wider rows.
-  // Results do not depend on the tiling (same K order per pixel).
-  {
-    auto tiles_of = [&](int wt, int r) {
-      return (long)((a->W + wt - 1) / wt) * ((a->H + r - 1) / r);
-    };
-    int bw = a->W < 128 ? a->W : 128;
-    int br = std::max(1, std::min(a->H, 128 / bw));
-    if (conv_tile_search_enabled()) {
-      for (int wt : {128, 64, 32, 16}) {
-        if (wt > a->W) continue;
-        const int r = std::max(1, std::min(a->H, 128 / wt));
-        if (tiles_of(wt, r) < tiles_of(bw, br)) {
-          bw = wt;
-          br = r;
-        }
-      }
-    }
-    p.Wt = bw;
-    p.R = br;
-  }
+  pixel_tile(a->H, a->W, &p.Wt, &p.R);
   p.x_tiles = (a->W + p.Wt - 1) / p.Wt;
   p.y_tiles = (a->H + p.R - 1) / p.R;
   p.n_tiles = a->Cout / bn;
@@ -673,6 +808,18 @@ extern "C" DDIT_API int ddit_conv(const ddit_conv_args* a, void* stream) {
   p.pix_tiles = a->B * a->T * p.y_tiles * p.x_tiles;
   p.pair_tiles = ((p.pix_tiles + 1) / 2) * p.n_tiles;
   p.bias = a->bias;
+  if (a->gn_part) {
+    const int G = a->gn_groups;
+    if (G < 1 || a->Cout % G || (a->Cout / G) % 2 || 64 % (a->Cout / G)) {
+      set_error("conv: GroupNorm statistics need Cout / groups in {2, 4, ..., 64} (Cout %d, groups %d)",
+                a->Cout, G);
+      return DDIT_E_INVALID;
+    }
+    p.gn_part = reinterpret_cast<float2*>(a->gn_part);
+    p.gn_G = G;
+    p.gn_cg = a->Cout / G;
+    p.gn_per_sample = a->gn_per_sample ? 1 : 0;
+  }
   CUtensorMap tx, tw, ty, tr;
   memset(&tr, 0, sizeof tr);
   bool ok = map_act(&tx, a->x, a->B, a->T, a->H, a->W, a->Cin, p.Wt, p.R) &&

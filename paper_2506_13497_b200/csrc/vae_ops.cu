@@ -504,6 +504,28 @@ DDIT_API int ddit_groupnorm(const void* x, void* y, double* stats, const float* 
   return check_cuda("groupnorm");
 }
 
+DDIT_API int ddit_groupnorm_partials(const void* x, void* y, const float* partial, int nblk,
+                                     float* coef, const float* gamma, const float* beta, int N,
+                                     int P, int C, int G, float eps, int silu_act, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (C % 8 || C % G || G > 32 || (C / 8) > 256 || 256 % (C / 8) || nblk < 1) {
+    set_error("groupnorm_partials: C a power of two in [8, 2048] divisible by G <= 32, nblk >= 1");
+    return DDIT_E_INVALID;
+  }
+  float2* cf = reinterpret_cast<float2*>(coef);
+  gn_finalize_kernel<<<dim3(N, (G + 7) / 8), 256, 0, s>>>(reinterpret_cast<const float2*>(partial), cf,
+                                                          gamma, beta, P, C, G, nblk, eps);
+  const size_t vpn = (size_t)P * (C / 8);
+  const dim3 grid((unsigned)((vpn + 256 * kGnUnroll - 1) / (256 * kGnUnroll)), N);
+  if (silu_act)
+    gn_apply_kernel<true><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                               static_cast<__nv_bfloat16*>(y), cf, C, vpn);
+  else
+    gn_apply_kernel<false><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                static_cast<__nv_bfloat16*>(y), cf, C, vpn);
+  return check_cuda("groupnorm_partials");
+}
+
 DDIT_API int ddit_upsample2x(const void* x, void* y, int N, int H, int W, int C, void* stream) {
   if (C % 8) {
     set_error("upsample2x: C %% 8 required");

@@ -96,9 +96,12 @@ def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
 
 
 def conv(x: torch.Tensor, w: torch.Tensor, *, bias: torch.Tensor | None = None,
-         residual: torch.Tensor | None = None, causal_time: bool = True, out=None, stream=None):
+         residual: torch.Tensor | None = None, causal_time: bool = True, out=None, stream=None,
+         gn_part: torch.Tensor | None = None, gn_groups: int = 0, gn_per_sample: bool = False):
     """Implicit-GEMM conv on tcgen05. x: [B,T,H,W,Cin] bf16 (channels-last);
-    w: [Cout,kt,kh,kw,Cin] bf16; returns [B,T,H,W,Cout] bf16."""
+    w: [Cout,kt,kh,kw,Cin] bf16; returns [B,T,H,W,Cout] bf16. ``gn_part`` (fp32, >= B*T*gn_groups*
+    nblk*2 floats, nblk = ddit_conv_frame_tiles(H, W)): per-frame (``gn_per_sample``: per-sample,
+    [B][G][T*nblk]) GroupNorm statistics partials of the output, written by the epilogue."""
     from ._lib import ConvArgs
 
     B, T, H, W, Cin = x.shape
@@ -108,5 +111,10 @@ def conv(x: torch.Tensor, w: torch.Tensor, *, bias: torch.Tensor | None = None,
         out = torch.empty(B, T, H, W, Cout, dtype=torch.bfloat16, device=x.device)
     a = ConvArgs(ptr(x), ptr(out), ptr(w), _c(bias), _c(residual), B, T, H, W, Cin, Cout, kt, kh,
                  kw, 1 if causal_time else 0)
+    if gn_part is not None:
+        assert gn_part.dtype == torch.float32 and gn_part.is_contiguous()
+        a.gn_part = ptr(gn_part)
+        a.gn_groups = gn_groups
+        a.gn_per_sample = 1 if gn_per_sample else 0
     check(lib().ddit_conv(ctypes.byref(a), stream_ptr(stream)))
     return out

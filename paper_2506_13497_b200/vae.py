@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
@@ -40,11 +41,22 @@ class VAEDecoder:
     """OpenSora-1.2 VAE decoder with device-resident weights on one GPU."""
 
     def __init__(self, cfg: VAEConfig, weights: dict[str, torch.Tensor], device="cuda:0",
-                 graphs: int = 0):
+                 graphs: int = 0, gn_from_conv: bool | None = None):
         """``graphs``: how many decode shapes keep a captured CUDA graph (0 = always eager). Off
         by default: a graph's private pool keeps every activation of the decode resident (720p:
-        ~150 GB) for ~3 % at 240p, where the kernels already hide the launch overhead."""
+        ~150 GB) for ~3 % at 240p, where the kernels already hide the launch overhead.
+        ``gn_from_conv``: GroupNorms of a convolution's output (per frame in the spatial decoder,
+        per clip in the temporal VAE) take their statistics from that convolution's epilogue (per
+        pixel tile, ``ddit_conv`` gn_part) instead of a statistics pass over the activation
+        (``ddit_groupnorm``); default on (env
+        DDIT_VAE_GN_CONV=0: off)."""
         self.cfg = cfg
+        if gn_from_conv is None:
+            gn_from_conv = os.environ.get("DDIT_VAE_GN_CONV", "1") != "0"
+        self.gn_from_conv = gn_from_conv
+        self._gn_src = None  # (conv output tensor, its statistics partials, nblk)
+        self._gn_bufs: list[torch.Tensor] = []  # partial buffers (kept alive: graphs hold them)
+        self.gn_coef = torch.empty(256 * 2048 * 2, dtype=torch.float32, device=device)
         self.max_graphs = graphs
         self._graphs: dict = {}
         self.dev = torch.device(device)
@@ -87,7 +99,18 @@ class VAEDecoder:
         self.launches = 0
 
     # ---------------------------------------------------------------- primitives
-    def _conv(self, x, name, *, residual=None, bias=True, causal=True, pad_bias=False):
+    def _gn_partials(self, n: int) -> torch.Tensor:
+        """A partial buffer of >= n floats (a new one when the current is too small; old ones stay
+        alive because captured graphs write to them)."""
+        if not self._gn_bufs or self._gn_bufs[-1].numel() < n:
+            self._gn_bufs.append(torch.empty(max(n, 1 << 20), dtype=torch.float32, device=self.dev))
+        return self._gn_bufs[-1]
+
+    def _conv(self, x, name, *, residual=None, bias=True, causal=True, pad_bias=False,
+              gn_stats=False):
+        """``gn_stats``: the epilogue also writes the GroupNorm statistics of y (per pixel tile;
+        per frame for the spatial, per clip for the causal temporal convs), which the next
+        ``_gn`` of exactly this tensor consumes."""
         B, T, H, Wd, Cin = x.shape
         w = self.bf[name + ".weight"]
         Cout, kt, kh, kw, _ = w.shape
@@ -96,7 +119,17 @@ class VAEDecoder:
         args = ConvArgs(ptr(x), ptr(y), ptr(w), ptr(b) if b is not None else None,
                         ptr(residual) if residual is not None else None, B, T, H, Wd, Cin, Cout, kt,
                         kh, kw, 1 if causal else 0)
+        gn = None
+        if gn_stats and self.gn_from_conv:
+            G = self.cfg.groups
+            nblk = lib().ddit_conv_frame_tiles(H, Wd) * (T if causal else 1)
+            part = self._gn_partials(B * T * G * nblk * 2 // (T if causal else 1))
+            args.gn_part = ptr(part)
+            args.gn_groups = G
+            args.gn_per_sample = 1 if causal else 0  # temporal VAE: GroupNorm over the whole clip
+            gn = (y, part, nblk, not causal)
         check(lib().ddit_conv(ctypes.byref(args), stream_ptr()))
+        self._gn_src = gn
         self.launches += 1
         return y
 
@@ -119,6 +152,14 @@ class VAEDecoder:
         B, T, H, Wd, C = x.shape
         N, P = (B * T, H * Wd) if per_frame else (B, T * H * Wd)
         y = torch.empty_like(x)
+        src = self._gn_src
+        if src is not None and src[0] is x and src[3] == per_frame:  # statistics from the conv epilogue
+            check(lib().ddit_groupnorm_partials(ptr(x), ptr(y), ptr(src[1]), src[2], ptr(self.gn_coef),
+                                                ptr(self.W[name + ".weight"]), ptr(self.W[name + ".bias"]),
+                                                N, P, C, self.cfg.groups, eps, 1 if silu else 0,
+                                                stream_ptr()))
+            self.launches += 2
+            return y
         check(lib().ddit_groupnorm(ptr(x), ptr(y), ptr(self.stats), ptr(self.W[name + ".weight"]),
                                    ptr(self.W[name + ".bias"]), N, P, C, self.cfg.groups, eps,
                                    1 if silu else 0, stream_ptr()))
@@ -129,10 +170,10 @@ class VAEDecoder:
     def _t_res(self, x, name):
         cfg = self.cfg
         h = self._gn(x, name + ".norm1", cfg.t_eps)
-        h = self._conv(h, name + ".conv1", bias=False)
+        h = self._conv(h, name + ".conv1", bias=False, gn_stats=True)
         h = self._gn(h, name + ".norm2", cfg.t_eps)
         res = x if (name + ".conv3.weight") not in self.W else self._conv(x, name + ".conv3", bias=False)
-        return self._conv(h, name + ".conv2", residual=res, bias=False)
+        return self._conv(h, name + ".conv2", residual=res, bias=False, gn_stats=True)
 
     def temporal_decode(self, z, t0: int, t1: int, num_frames: int) -> torch.Tensor:
         """Latent frames [t0, t1) of z [1, 4, T, h, w] (fp32, channels-first) ->
@@ -163,15 +204,16 @@ class VAEDecoder:
         return x[:, tpad:]
 
     # ---------------------------------------------------------------- spatial VAE
-    def _s_res(self, x, name):
+    def _s_res(self, x, name, stats_out=True):
+        """``stats_out``: a per-frame GroupNorm consumes the output (conv2 writes its statistics)."""
         cfg = self.cfg
         h = self._gn(x, name + ".norm1", cfg.sd_eps, per_frame=True)
-        h = self._conv(h, name + ".conv1", causal=False)
+        h = self._conv(h, name + ".conv1", causal=False, gn_stats=True)
         h = self._gn(h, name + ".norm2", cfg.sd_eps, per_frame=True)
         res = x
         if (name + ".conv_shortcut.weight") in self.W:
             res = self._conv(x, name + ".conv_shortcut", causal=False)
-        return self._conv(h, name + ".conv2", residual=res, causal=False)
+        return self._conv(h, name + ".conv2", residual=res, causal=False, gn_stats=stats_out)
 
     def _mid_attention(self, x):
         cfg = self.cfg
@@ -219,13 +261,14 @@ class VAEDecoder:
         n = len(cfg.block_out)
         for i in range(n):
             for j in range(cfg.layers_per_block + 1):
-                x = self._s_res(x, f"s.up.{i}.resnets.{j}")
+                x = self._s_res(x, f"s.up.{i}.resnets.{j}",
+                                stats_out=i == n - 1 or j < cfg.layers_per_block)
             if i < n - 1:
                 B, T, H, Wd, C = x.shape
                 up = torch.empty((B, T, 2 * H, 2 * Wd, C), dtype=torch.bfloat16, device=self.dev)
                 check(lib().ddit_upsample2x(ptr(x), ptr(up), B * T, H, Wd, C, stream_ptr()))
                 self.launches += 1
-                x = self._conv(up, f"s.up.{i}.upsample", causal=False)
+                x = self._conv(up, f"s.up.{i}.upsample", causal=False, gn_stats=True)
         x = self._gn(x, "s.norm_out", cfg.sd_eps, per_frame=True)
         y = self._conv(x, "s.conv_out", causal=False, pad_bias=True)  # [N, 1, H, W, 64]
         B, T, H, Wd, C = y.shape
