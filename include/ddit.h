@@ -56,12 +56,6 @@ DDIT_API int ddit_set_gemm_wide(int on);
 /* QKV GEMM on per-head padded weights (80-row head slots, 256 x 240 tiles; default 1; env
  * DDIT_QKV_PAD=0); bit-identical results. Applies to requests opened afterwards. */
 DDIT_API int ddit_set_qkv_pad(int on);
-/* Keep the request's fp32 residual stream (x, 56 MB at 240p DoP 1) resident in L2: a persisting
- * carve-out of its size (up to the device maximum) at request open and an access-policy window
- * over it on the step's stream at every ddit_step_begin (graphs captured from the stream carry
- * it). Default 1 (env DDIT_L2_RESID=0); no effect on results. Applies to requests opened
- * afterwards. */
-DDIT_API int ddit_set_l2_resident(int on);
 /* VAE convolutions as cta_group::2 pairs of 128-pixel tiles (half the weight rows per CTA) when
  * there are enough tiles (default 1; env DDIT_CONV_2CTA=0); bit-identical results. */
 DDIT_API int ddit_set_conv_2cta(int on);

@@ -129,7 +129,6 @@ _SIGNATURES = {
     "ddit_set_gemm_2cta": [ci],
     "ddit_set_gemm_wide": [ci],
     "ddit_set_qkv_pad": [ci],
-    "ddit_set_l2_resident": [ci],
     "ddit_set_conv_2cta": [ci],
     "ddit_set_conv_tile_search": [ci],
     "ddit_set_pdl": [ci],

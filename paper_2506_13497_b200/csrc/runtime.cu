@@ -189,11 +189,6 @@ struct ddit_req {
   bool external_xch = false;     // the caller moves the rows (staged pack -> ncclAllToAll -> unpack)
   // profiling: event pairs around every launch, tagged by kernel class
   bool prof_on = false;
-  // L2 access-policy window over the fp32 residual stream (x_sp, x_tp): set on the step's stream
-  // at every ddit_step_begin (captured graphs inherit it), l2_bytes = 0: off
-  void* l2_base = nullptr;
-  size_t l2_bytes = 0;
-  float l2_hit = 1.f;
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_cls;
   size_t ev_n = 0;
@@ -639,22 +634,6 @@ DDIT_API int ddit_model_create(const ddit_config* cfg, const ddit_weights* w, dd
   return DDIT_OK;
 }
 
-// residual stream held in L2 (env DDIT_L2_RESID=0 / ddit_set_l2_resident(0): off); applies to
-// requests opened afterwards
-static int g_l2_resid = -1;
-static bool l2_resident_enabled() {
-  if (g_l2_resid < 0) {
-    const char* e = getenv("DDIT_L2_RESID");
-    g_l2_resid = (e && e[0] == '0') ? 0 : 1;
-  }
-  return g_l2_resid != 0;
-}
-
-DDIT_API int ddit_set_l2_resident(int on) {
-  g_l2_resid = on ? 1 : 0;
-  return DDIT_OK;
-}
-
 DDIT_API int ddit_set_qkv_pad(int on) {
   g_qkv_pad = on ? 1 : 0;
   return DDIT_OK;
@@ -789,30 +768,6 @@ DDIT_API int ddit_request_open(ddit_model* m, const ddit_req_desc* d, void* work
   r->ws = ws;
   r->x_sp = reinterpret_cast<float*>(ws + r->L.x_sp);
   r->x_tp = reinterpret_cast<float*>(ws + r->L.x_tp);
-  if (l2_resident_enabled()) {
-    // x_sp and x_tp are adjacent in the layout: one window over both, a persisting carve-out of
-    // that size (as far as the device allows; the carve-out serves normal accesses while no
-    // persisting lines occupy it), hit ratio = carve-out / window when the window is larger
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, r->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0) {
-      const size_t x_bytes = (size_t)std::max(g.M_sp, 1) * m->cfg.hidden * 4;
-      const size_t span = r->L.x_tp == r->L.x_sp ? x_bytes
-                                                 : (size_t)(r->L.x_tp - r->L.x_sp) +
-                                                       (size_t)std::max(g.M_tp, 1) * m->cfg.hidden * 4;
-      const size_t win = std::min(span, (size_t)prop.accessPolicyMaxWindowSize);
-      size_t carve = 0;
-      cudaDeviceGetLimit(&carve, cudaLimitPersistingL2CacheSize);
-      const size_t want = std::min(win, (size_t)prop.persistingL2CacheMaxSize);
-      if (carve < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
-        carve = want;
-      if (carve > 0) {
-        r->l2_base = r->x_sp;
-        r->l2_bytes = win;
-        r->l2_hit = std::min(1.f, (float)carve / (float)win);
-      }
-    }
-    cudaGetLastError();
-  }
   r->xb = reinterpret_cast<bf16*>(ws + r->L.xb);
   r->xm = reinterpret_cast<bf16*>(ws + r->L.xm);
   r->big = reinterpret_cast<bf16*>(ws + r->L.big);
@@ -1038,19 +993,6 @@ DDIT_API int ddit_step_begin(ddit_req* r, const float* z_local, int step, void* 
   const ddit_weights& w = m->w;
   const Geometry& g = r->g;
   const int C = c.hidden, B = g.B;
-  if (r->l2_bytes) {  // the residual stream stays in L2 across the step's kernels
-    cudaStreamAttrValue v;
-    memset(&v, 0, sizeof v);
-    v.accessPolicyWindow.base_ptr = r->l2_base;
-    v.accessPolicyWindow.num_bytes = r->l2_bytes;
-    v.accessPolicyWindow.hitRatio = r->l2_hit;
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
-      cudaGetLastError();
-      r->l2_bytes = 0;
-    }
-  }
   // t / fps embedding -> t (temb) -> t_block (tmlp)
   return timed(r, K_EW, s, 8, [&] {
   timestep_freq(r->freq, r->tv + 4 * step, 2 * B, c.freq_dim, s);
