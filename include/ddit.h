@@ -121,7 +121,6 @@ typedef struct ddit_attn {
   float scale;
 } ddit_attn;
 
-DDIT_API int ddit_attention(const ddit_attn* a, void* stream);
 /* Temporal attention (T <= 64 frames; tcgen05): q/k/v must be the three sections of one
  * row-major QKV matrix and share one index map (heads of one position stacked into 128-row tiles). */
 DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
@@ -271,8 +270,8 @@ DDIT_API int ddit_set_exchange_timeout_ms(int ms);
 DDIT_API int ddit_request_timestep(const ddit_req* r, int step, float* t, float* dt);
 
 /* Request options: DDIT_OPT_TC_ATTENTION is retired -- spatial / cross attention always run the
- * tcgen05 FMHA (value 1 is accepted, 0 returns DDIT_E_INVALID; the mma.sync flash kernel is
- * reachable only through ddit_attention, as a test cross-check). */
+ * tcgen05 FMHA (value 1 is accepted, 0 returns DDIT_E_INVALID; there is no other attention
+ * kernel). */
 #define DDIT_OPT_TC_ATTENTION 1
 /* DDIT_OPT_EXTERNAL_XCH (default 0): the step does not exchange rows itself (no peers, no fused
  * fc2 stores, no flag barrier); after every ddit_step_phase the caller moves them with

@@ -136,7 +136,6 @@ _SIGNATURES = {
     "ddit_set_resid_reduce": [ci],
     "ddit_set_exchange_timeout_ms": [ci],
     "ddit_enable_peer_access": [ci, ci],
-    "ddit_attention": [ctypes.POINTER(Attn), vp],
     "ddit_attention_temporal": [ctypes.POINTER(Attn), vp],
     "ddit_attention_tc": [ctypes.POINTER(Attn), vp],
     "ddit_ln_modulate": [vp, vp, ci, ci, vp, vp, ci, ci, ctypes.c_float, vp],

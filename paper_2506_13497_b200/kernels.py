@@ -78,8 +78,12 @@ def gemm(
 
 def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
               q_map=(1, 0, 0, 1), kv_map=(1, 0, 0, 1), scale: float | None = None, stream=None,
-              temporal: bool = False, tc: bool = False):
-    """Flash attention over token-major bf16 matrices; maps = (inner, outer, inner_stride, tok)."""
+              temporal: bool = False, tc: bool = True):
+    """Attention over token-major bf16 matrices; maps = (inner, outer, inner_stride, tok): the
+    tcgen05 FMHA (spatial / cross) or, with ``temporal``, the tcgen05 temporal kernel (q/k/v the
+    three sections of one QKV matrix, T <= 64). ``tc`` is kept for callers; it must be True."""
+    if not tc:
+        raise ValueError("the mma.sync attention kernel was removed; only the tcgen05 kernels exist")
     a = Attn()
     a.q, a.ldq = ptr(q), q.stride(0)
     a.k, a.ldk = ptr(k), k.stride(0)
@@ -89,8 +93,7 @@ def attention(q, k, v, o, *, heads: int, num_seqs: int, Lq: int, Lk: int,
     a.q_inner, a.q_outer, a.q_inner_stride, a.q_tok = q_map
     a.kv_inner, a.kv_outer, a.kv_inner_stride, a.kv_tok = kv_map
     a.scale = scale if scale is not None else 72 ** -0.5
-    fn = (lib().ddit_attention_temporal if temporal else
-          lib().ddit_attention_tc if tc else lib().ddit_attention)
+    fn = lib().ddit_attention_temporal if temporal else lib().ddit_attention_tc
     check(fn(ctypes.byref(a), stream_ptr(stream)))
     return o
 
