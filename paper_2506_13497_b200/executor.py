@@ -21,7 +21,8 @@ allocator / policy decision stays the reference's.
   takes a pooled group for the new GPU set and broadcasts the text state from the old rank 0
   (``ddit_request_copy_text``) together with the latent re-shard, which is what the reference's
   broadcast + scale-up constants stand for. ``reshard_seconds`` is that device work (CUDA events,
-  max over the new ranks when the group is emulated); ``reshard_host_seconds`` the host wall time.
+  max over the new ranks when the group is emulated); ``reshard_host_seconds`` the host work of
+  the promotion (re-bind + enqueue), ``reshard_wall_seconds`` the wall time including the device wait.
 * ``profile_b200`` measures ``dit_step_seconds`` per (resolution, DoP) and emits the
   reference's ``dit-profile/1`` document (profiles.py:132-215).
 """
@@ -144,8 +145,11 @@ class B200Executor:
         self.pool: dict[tuple, list[_Live]] = {}  # (resolution, devices) -> idle groups
         self.pool_limit = 4
         self._enqueue_pool: ThreadPoolExecutor | None = None  # per-rank step enqueue threads
-        self.reshard_host_seconds: list[float] = []  # promotion wall time, device wait included
-        self.reshard_enqueue_seconds: list[float] = []  # host work to enqueue the re-shard
+        # host work of a promotion: pool re-bind + enqueue of the one-call re-shard on every rank
+        self.reshard_host_seconds: list[float] = []
+        # wall time until the re-shard finished (host + device wait); with emulated groups the
+        # virtual ranks' re-shards run one after another on one GPU, so this grows with P' there
+        self.reshard_wall_seconds: list[float] = []
         # when set, every request's denoised latent (+ frames with keep_videos) is also written
         # in the latent_io on-disk format as the DiT group hands it off
         self.latent_dir = latent_dir
@@ -267,8 +271,8 @@ class B200Executor:
             # ranks on P GPUs re-shard concurrently; virtual ranks on one device ran one by one
             dev_s = max(per) if (self.emulate_group or not one_device) else sum(per)
             self.reshard_seconds.append(dev_s)
-            self.reshard_host_seconds.append(time.perf_counter() - t0)
-            self.reshard_enqueue_seconds.append(t_enq - t0)
+            self.reshard_wall_seconds.append(time.perf_counter() - t0)
+            self.reshard_host_seconds.append(t_enq - t0)
             new.steps_done = live.steps_done
             new.history = live.history + [live.gpu_ids]
             self._close(live)
