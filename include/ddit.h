@@ -130,8 +130,9 @@ DDIT_API int ddit_attention_temporal(const ddit_attn* a, void* stream);
 DDIT_API int ddit_ln_modulate(const float* x, void* out_bf16, int M, int C, const float* shift,
                               const float* scale, int mod_stride, int rows_per_b, float eps,
                               void* stream);
-/* LN kernel variant for launches made afterwards (tuning): 1 one warp per row, 3 (default)
- * persistent streaming warps (C = 1152; other widths take the generic kernel). Env DDIT_LN. */
+/* LN kernel variant for launches made afterwards (tuning): 1 one warp per row, 3 persistent
+ * streaming warps, 5 (default) streaming warps with the modulation held in registers (C = 1152;
+ * other widths take the generic kernel); all bit-identical. Env DDIT_LN. */
 DDIT_API int ddit_set_ln_variant(int variant);
 /* tcgen05 / TMEM flash attention (spatial and cross attention): contiguous sequences
  * (tok == 1, inner <= 1), row strides and head offsets in whole 72-column slots, k and v in one

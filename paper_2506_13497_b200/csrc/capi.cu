@@ -92,7 +92,7 @@ DDIT_API int ddit_ln_modulate(const float* x, void* out_bf16, int M, int C, cons
   return check_cuda("ln_modulate");
 }
 DDIT_API int ddit_set_ln_variant(int variant) {
-  if (variant != 0 && variant != 1 && variant != 2 && variant != 3) {
+  if (variant < 0 || variant > 5 || variant == 4) {
     set_error("ddit_set_ln_variant: unknown variant %d", variant);
     return DDIT_E_INVALID;
   }

@@ -133,9 +133,77 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Variant 5: the streaming kernel with the row's modulation (shift, scale: 18 float4 per lane)
+// held in registers and reloaded only when the warp's batch index changes, so a row costs the
+// L1 4.6 KB of x + 2.3 KB of stores instead of + 9.2 KB of modulation loads. Same arithmetic.
+__global__ void __launch_bounds__(128)
+    ln_modulate_stream_regmod_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out,
+                                     int M, const float* __restrict__ shift,
+                                     const float* __restrict__ scale, int mod_stride,
+                                     int rows_per_b, float eps) {
+  constexpr int C = 1152, NV = 9;
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= M) return;
+  float4 v[NV], sh[NV], sc[NV];
+  int cur_b = -1;
+  {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = __ldcs(xr + lane + 32 * i);
+  }
+  for (;;) {
+    const int next = row + nw;
+    float4 nx[NV];
+    if (next < M) {
+      const float4* xr = reinterpret_cast<const float4*>(x + (size_t)next * C);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) nx[i] = __ldcs(xr + lane + 32 * i);
+    }
+    const int bidx = row / rows_per_b;
+    if (bidx != cur_b) {
+      cur_b = bidx;
+      const float4* a = reinterpret_cast<const float4*>(shift + (size_t)bidx * mod_stride);
+      const float4* k = reinterpret_cast<const float4*>(scale + (size_t)bidx * mod_stride);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        sh[i] = __ldg(a + lane + 32 * i);
+        sc[i] = __ldg(k + lane + 32 * i);
+      }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = group_sum<32>(s) * (1.f / C);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
+    const float rstd = rsqrtf(group_sum<32>(q) * (1.f / C) + eps);
+    uint2* o = reinterpret_cast<uint2*>(out + (size_t)row * C);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float y0 = (v[i].x - mean) * rstd * (1.f + sc[i].x) + sh[i].x;
+      const float y1 = (v[i].y - mean) * rstd * (1.f + sc[i].y) + sh[i].y;
+      const float y2 = (v[i].z - mean) * rstd * (1.f + sc[i].z) + sh[i].z;
+      const float y3 = (v[i].w - mean) * rstd * (1.f + sc[i].w) + sh[i].w;
+      o[lane + 32 * i] = make_uint2(pack_bf16(y0, y1), pack_bf16(y2, y3));
+    }
+    if (next >= M) break;
+    row = next;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = nx[i];
+  }
+}
+
 static int g_ln_variant = -1;  // tuning hook (env DDIT_LN): 0 generic, 1 = 32 lanes x 9, 2 = 16 x 18,
-                               // 3 (default; 240p: 12 vs 17 us hot, 14 vs 19 cold, scripts/ln_bench.py)
-                               // 3 = persistent streaming warps
+                               // 3 = persistent streaming warps (240p: 11.3 / 14.2 us hot / cold),
+                               // 5 (default) = 3 with the modulation in registers (9.3 / 12.2 us;
+                               // scripts/ln_bench.py, profiles/r02_ln_regmod_bench.txt)
 
 void set_ln_variant(int v) { g_ln_variant = v; }
 
@@ -144,7 +212,7 @@ int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* s
   if (C % 4 || C > 32 * 4 * kMaxVec || M <= 0) return -2;
   if (g_ln_variant < 0) {
     const char* e = getenv("DDIT_LN");
-    g_ln_variant = e ? atoi(e) : 3;
+    g_ln_variant = e ? atoi(e) : 5;
   }
   const int rpb = rows_per_b > 0 ? rows_per_b : M;
   if (C == 1152 && g_ln_variant == 3) {
@@ -161,6 +229,18 @@ int ln_modulate(const float* x, __nv_bfloat16* out, int M, int C, const float* s
     const int need = (M + 7) / 8;
     launch_pdl(ln_modulate_stream_kernel, dim3(need < grid_cap ? need : grid_cap), dim3(256), 0, s,
                x, out, M, shift, scale, mod_stride, rpb, eps);
+  } else if (C == 1152 && g_ln_variant == 5) {
+    static int grid_cap = 0;
+    if (!grid_cap) {
+      int dev = 0, sms = 148, bps = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ln_modulate_stream_regmod_kernel, 128, 0);
+      grid_cap = sms * (bps > 0 ? bps : 1);
+    }
+    const int need = (M + 3) / 4;
+    launch_pdl(ln_modulate_stream_regmod_kernel, dim3(need < grid_cap ? need : grid_cap), dim3(128),
+               0, s, x, out, M, shift, scale, mod_stride, rpb, eps);
   } else if (C == 1152 && g_ln_variant == 1) {
     launch_pdl(ln_modulate_kernel<9, 32, true>, dim3((M + 3) / 4), dim3(128), 0, s, x, out, M, C,
                shift, scale, mod_stride, rpb, eps);

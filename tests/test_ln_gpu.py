@@ -6,7 +6,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("variant", [1, 3, 5])
 @pytest.mark.parametrize("M,C,nb", [(12150, 1152, 2), (1519, 1152, 2), (37, 1152, 3), (300, 288, 2)])
 def test_ln_modulate_matches_torch(cuda, variant, M, C, nb):
     from paper_2506_13497_b200 import _lib
@@ -24,9 +24,35 @@ def test_ln_modulate_matches_torch(cuda, variant, M, C, nb):
                                       scale.data_ptr(), 6 * C, rpb, 1e-6,
                                       torch.cuda.current_stream().cuda_stream))
     finally:
-        L.ddit_set_ln_variant(3)
+        L.ddit_set_ln_variant(5)
     torch.cuda.synchronize()
     b = torch.arange(M, device=cuda) // rpb
     ref = torch.nn.functional.layer_norm(x, (C,), eps=1e-6) * (1 + scale[b]) + shift[b]
     err = ((out.float() - ref).norm() / ref.norm()).item()
     assert err < 4e-3, err
+
+
+@pytest.mark.parametrize("M", [12150, 1519, 37, 5])
+def test_ln_register_modulation_bit_identical_to_streaming(cuda, M):
+    """Variant 5 (modulation held in registers, reloaded when the batch index changes) computes
+    exactly what the streaming kernel computes, including rows on both sides of a batch edge."""
+    from paper_2506_13497_b200 import _lib
+
+    L = _lib.lib()
+    C = 1152
+    g = torch.Generator(device=cuda).manual_seed(M)
+    x = 3 * torch.randn(M, C, device=cuda, generator=g) + 0.5
+    mods = torch.randn(3, 6, C, device=cuda, generator=g)
+    outs = []
+    try:
+        for v in (3, 5):
+            out = torch.full((M, C), float("nan"), device=cuda, dtype=torch.bfloat16)
+            _lib.check(L.ddit_set_ln_variant(v))
+            _lib.check(L.ddit_ln_modulate(x.data_ptr(), out.data_ptr(), M, C, mods[:, 0].data_ptr(),
+                                          mods[:, 1].data_ptr(), 6 * C, -(-M // 3), 1e-6,
+                                          torch.cuda.current_stream().cuda_stream))
+            outs.append(out)
+    finally:
+        L.ddit_set_ln_variant(5)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
